@@ -1,0 +1,134 @@
+/*
+ * simplex_asm_b200.h -- C ABI of the B200-native P1 assembly path.
+ *
+ * This is the drop-in boundary for the reference's assembly drivers
+ * (reference = /root/reference/pkg/src/simplex_asm).  The reference is pure
+ * Python; its "FFI" for this path is the Python driver protocol
+ *     driver(mesh: Mesh, kernel) -> SparseMatrix        assembly.py:295-308
+ * The Python package paper_1401_3301_b200 binds these symbols with ctypes
+ * (INTEGRATION.md shows the binding) and re-exposes that protocol.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Pointers named *_dev are CUDA device
+ *     pointers on `device`; `stream` is a cudaStream_t (NULL = legacy default).
+ *   - Every entry point returns an sa_status; 0 = success.  On failure
+ *     sa_last_error() gives a thread-local message and sa_bad_index() the
+ *     element / position the reference would name in its exception.
+ *   - Results are bitwise deterministic run to run.
+ */
+#ifndef SIMPLEX_ASM_B200_H
+#define SIMPLEX_ASM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum sa_status {
+    SA_OK = 0,
+    SA_ERR_DEGENERATE = 1,   /* -> DegenerateSimplexError(element)   errors.py:12-17, kernels.py:60-62 */
+    SA_ERR_INDEX_RANGE = 2,  /* -> IndexRangeError                   errors.py:20-21, mesh.py:83-87 */
+    SA_ERR_CAPACITY = 3,     /* -> CapacityError                     errors.py:8-9 */
+    SA_ERR_ARG = 4,          /* -> ValueError                        */
+    SA_ERR_CUDA = 5,         /* -> RuntimeError (CUDA error text)    */
+    SA_ERR_NOMEM = 6         /* -> MemoryError                       */
+} sa_status;
+
+/* Operators (bit mask: MASS|STIFF may be fused into one numeric pass). */
+enum {
+    SA_OP_MASS = 1,      /* MassKernel       kernels.py:281-303 (mass_kernel :68-78)      */
+    SA_OP_STIFF = 2,     /* StiffnessKernel  kernels.py:306-329 (stiffness_kernel :81-88) */
+    SA_OP_ELASTIC = 4,   /* ElasticKernel    kernels.py:332-387 (elastic_kernel :155-172) */
+    SA_OP_GENERAL = 8    /* -div(A grad u)+div(b u)+c.grad u+a0 u */
+};
+
+/* OpenBLAS kernel family whose dgesv/dgetrf bits the gradients reproduce
+ * (kernels.py:64 -> numpy -> OpenBLAS). */
+enum { SA_CORE_SKYLAKEX = 0, SA_CORE_HASWELL = 1 };
+
+typedef struct sa_mesh sa_mesh;   /* device-resident mesh (Mesh, mesh.py:46-101) */
+typedef struct sa_plan sa_plan;   /* symbolic phase for one dof-row block        */
+
+/* ---- mesh ------------------------------------------------------------- */
+
+/* Upload-side mesh construction, replacing Mesh.from_arrays (mesh.py:54-58)
+ * + compute_volumes (mesh.py:29-43).
+ *   q_dev    (d, nq) f64 row-major, the reference layout of Mesh.q
+ *   me_dev   (d+1, nme) int64 row-major (Mesh.me); checked against [0, nq)
+ *            -> SA_ERR_INDEX_RANGE, sa_bad_index() = a*nme + k of the first
+ *            bad entry in row-major order (mesh.py:83-87 names me[a, k]).
+ *   vols_dev (nme,) f64 Mesh.vols, or NULL: volumes are then computed on the
+ *            device from the numpy-det factorisation (mesh.py:38-43); zero
+ *            volume -> SA_ERR_DEGENERATE with the first element.
+ * The mesh keeps private device copies (q as padded AoS, me as int32). */
+int sa_mesh_create(int d, int64_t nq, int64_t nme, const double *q_dev, const int64_t *me_dev,
+                   const double *vols_dev, int core, int device, void *stream, sa_mesh **out);
+int sa_mesh_vols(const sa_mesh *mesh, double *vols_dev_out, void *stream);
+int sa_mesh_destroy(sa_mesh *mesh);
+
+/* ---- symbolic phase (once per mesh and row block) ---------------------- */
+
+/* Pattern of dof rows [row_begin, row_end) of an m-unknowns-per-node system
+ * (m = 1 scalar, m = d elastic; interleaved dofs r = m*i + l, assembly.py:181-183).
+ * row_begin/row_end must be multiples of m.  Replaces the structural part of
+ * _canonicalize (sparse.py:91-115): node->element incidences in ascending
+ * element order, sorted unique columns per row, indptr.  The structural
+ * pattern is the optv2 pattern before exact-zero sums are dropped. */
+int sa_plan_create(const sa_mesh *mesh, int m, int64_t row_begin, int64_t row_end, void *stream,
+                   sa_plan **out);
+/* nrows = row_end - row_begin; nnz = structural entries of the block. */
+int sa_plan_info(const sa_plan *plan, int64_t *nrows, int64_t *nnz_structural,
+                 int64_t *max_row_nodes);
+/* Structural CSR of the block (indptr relative, int64 (nrows+1); indices
+ * global column dofs int32 (nnz)), into caller-allocated device buffers. */
+int sa_plan_pattern(const sa_plan *plan, int64_t *indptr_dev, int32_t *indices_dev, void *stream);
+int sa_plan_destroy(sa_plan *plan);
+
+/* ---- numeric phase (repeated for new coefficients) --------------------- */
+
+/* Nodal coefficients (device pointers, nq entries unless stated) or
+ * constants when the pointer is NULL -- the values _nodal_values produces
+ * (kernels.py:268-278). */
+typedef struct sa_coeffs {
+    const double *w;     double w_const;      /* mass weight               */
+    const double *lamb;  double lamb_const;   /* Lame lambda (elastic)     */
+    const double *mu;    double mu_const;     /* Lame mu (elastic)         */
+    const double *A;     /* general: (nq, d, d) row-major; NULL = A_const  */
+    const double *b;     /* general: (nq, d); NULL = 0                     */
+    const double *c;     /* general: (nq, d); NULL = 0                     */
+    const double *a0;    /* general: (nq,);  NULL = a0_const               */
+    double A_const[9];
+    double a0_const;
+} sa_coeffs;
+
+/* Assemble the values of every structural entry of the block into
+ * vals_dev[k] (k-th op in ascending SA_OP bit order, each nnz_structural
+ * doubles, so MASS|STIFF writes mass at vals_dev[0] and stiffness at
+ * vals_dev[1]).  Each entry is the left-to-right sum of its element
+ * contributions in ascending element order -- bitwise the optv2 value
+ * (assembly.py:92-111, sparse.py:97-106).  n_zero_out[k] = number of
+ * structural entries whose sum is exactly +-0.0 (sparse.py:108-111 drops
+ * them; see sa_compact).  q is read from the mesh; vols too.
+ * Degenerate element (zero pivot) -> SA_ERR_DEGENERATE, sa_bad_index() = the
+ * smallest such element (kernels.py:59-62). */
+int sa_numeric(sa_plan *plan, int ops, const sa_coeffs *coeffs, double *const *vals_dev,
+               int64_t *n_zero_out, void *stream);
+
+/* Drop exact-zero entries (sparse.py:108-111) from one op's values:
+ * writes the canonical block CSR (indptr_out relative int64, indices_out
+ * int32, vals_out f64, sized from sa_numeric's n_zero). */
+int sa_compact(const sa_plan *plan, const double *vals_dev, int64_t *indptr_out_dev,
+               int32_t *indices_out_dev, double *vals_out_dev, void *stream);
+
+/* ---- diagnostics ------------------------------------------------------- */
+const char *sa_last_error(void);
+int64_t sa_bad_index(void);
+/* Number of sa_* kernel launches issued by this thread since the last reset
+ * (bench.py's gpu_launches). */
+int64_t sa_launch_count(int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,125 @@
+// sa_scan.cu -- device-wide exclusive scan (int64) and error plumbing.
+#include <cstdarg>
+#include <cstdio>
+
+#include "sa_common.cuh"
+
+namespace sa {
+
+ErrState &err_state()
+{
+    static thread_local ErrState s;
+    return s;
+}
+
+int set_error(int status, const char *fmt, ...)
+{
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    err_state().msg = buf;
+    return status;
+}
+
+namespace {
+constexpr int SCAN_BLOCK = 512;
+constexpr int SCAN_ITEMS = 8;
+constexpr int64_t SCAN_TILE = (int64_t)SCAN_BLOCK * SCAN_ITEMS;
+
+__device__ __forceinline__ int64_t warp_incl_scan(int64_t v)
+{
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int64_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// exclusive block scan of one value per thread; returns the block total in *total
+__device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t *total)
+{
+    __shared__ int64_t warp_sums[SCAN_BLOCK / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int64_t inc = warp_incl_scan(v);
+    if (lane == 31) warp_sums[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        int64_t s = lane < SCAN_BLOCK / 32 ? warp_sums[lane] : 0;
+        s = warp_incl_scan(s);
+        if (lane < SCAN_BLOCK / 32) warp_sums[lane] = s;
+    }
+    __syncthreads();
+    int64_t base = wid ? warp_sums[wid - 1] : 0;
+    *total = warp_sums[SCAN_BLOCK / 32 - 1];
+    __syncthreads();
+    return base + inc - v;
+}
+
+__global__ void __launch_bounds__(SCAN_BLOCK) k_scan_reduce(const int64_t *__restrict__ in, int64_t n,
+                                                            int64_t *__restrict__ sums)
+{
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+    int64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        int64_t idx = base + (int64_t)i * SCAN_BLOCK + threadIdx.x;
+        if (idx < n) s += in[idx];
+    }
+    int64_t tot;
+    block_excl_scan(s, &tot);
+    if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+// each thread owns SCAN_ITEMS consecutive items of the tile
+__global__ void __launch_bounds__(SCAN_BLOCK) k_scan_tiles(const int64_t *in, int64_t *out, int64_t n,
+                                                           const int64_t *__restrict__ offs)
+{
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    int64_t v[SCAN_ITEMS];
+    int64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        v[i] = (base + i < n) ? in[base + i] : 0;
+        s += v[i];
+    }
+    int64_t tot;
+    int64_t run = block_excl_scan(s, &tot) + (offs ? offs[blockIdx.x] : 0);
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        if (base + i < n) out[base + i] = run;
+        run += v[i];
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = (offs ? offs[blockIdx.x] : 0) + tot;
+}
+}  // namespace
+
+int64_t scan_tmp_elems(int64_t n)
+{
+    if (n <= SCAN_TILE) return 1;
+    int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+    return (nb + 1) + scan_tmp_elems(nb);
+}
+
+int exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t n, int64_t *tmp, cudaStream_t st)
+{
+    if (n <= 0) {
+        SA_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(int64_t), st));
+        return SA_OK;
+    }
+    if (n <= SCAN_TILE) {
+        SA_LAUNCH(k_scan_tiles, 1, SCAN_BLOCK, 0, st, in, out, n, (const int64_t *)nullptr);
+        return SA_OK;
+    }
+    int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+    int64_t *sums = tmp;
+    SA_LAUNCH(k_scan_reduce, (unsigned)nb, SCAN_BLOCK, 0, st, in, n, sums);
+    SA_TRY(exclusive_scan_i64(sums, sums, nb, tmp + nb + 1, st));
+    SA_LAUNCH(k_scan_tiles, (unsigned)nb, SCAN_BLOCK, 0, st, in, out, n, (const int64_t *)sums);
+    return SA_OK;
+}
+
+}  // namespace sa

@@ -1,0 +1,271 @@
+"""Device layer: torch CUDA buffers around the C ABI (include/simplex_asm_b200.h).
+
+PyTorch is used for device memory, streams and transfers only; every
+numeric step runs in the sm_100a library.  There is no CPU fallback: without
+CUDA or the library these classes raise ExtensionMissingError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import ExtensionMissingError
+
+try:
+    import torch
+except Exception as exc:  # pragma: no cover
+    raise ExtensionMissingError(f"torch is required for device buffers: {exc}") from exc
+
+OP_BITS = {"mass": _lib.SA_OP_MASS, "stiffness": _lib.SA_OP_STIFF, "elastic": _lib.SA_OP_ELASTIC,
+           "general": _lib.SA_OP_GENERAL}
+
+
+def _require_cuda(device):
+    if not torch.cuda.is_available():
+        raise ExtensionMissingError("no CUDA device: the B200 assembly path has no CPU fallback")
+    return torch.device(device if device is not None else f"cuda:{torch.cuda.current_device()}")
+
+
+def _stream_ptr(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _to_dev(x, dtype, device):
+    if isinstance(x, torch.Tensor):
+        return x.to(device=device, dtype=dtype, non_blocking=True).contiguous()
+    t = torch.from_numpy(np.ascontiguousarray(x))
+    return t.to(device=device, dtype=dtype, non_blocking=True).contiguous()
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+class DeviceMesh:
+    """A mesh resident on one B200: q (padded AoS f64), me (int32 AoS), vols.
+
+    ``q`` (d, nq) and ``me`` (d+1, nme) are host arrays (numpy, the reference
+    layout) or CUDA tensors.  ``vols=None`` computes volumes on the device.
+    """
+
+    def __init__(self, q, me, vols=None, *, core: str = "SkylakeX", device=None, stream=None):
+        dev = _require_cuda(device)
+        L = _lib.load()
+        self.device = dev
+        self.core = core
+        with torch.cuda.device(dev):
+            qd = _to_dev(q, torch.float64, dev)
+            med = _to_dev(me, torch.int64, dev)
+            vd = _to_dev(vols, torch.float64, dev) if vols is not None else None
+            self.d, self.nq = int(qd.shape[0]), int(qd.shape[1])
+            self.nme = int(med.shape[1]) if med.dim() == 2 else 0
+            if med.shape[0] != self.d + 1:
+                raise ValueError(f"connectivity shape {tuple(med.shape)} does not match ({self.d + 1}, nme)")
+            h = ctypes.c_void_p()
+            rc = L.sa_mesh_create(self.d, self.nq, self.nme, _ptr(qd), _ptr(med), _ptr(vd), _lib.SA_CORE[core],
+                                  dev.index, _stream_ptr(stream), ctypes.byref(h))
+            _lib.check(rc)
+        self._h = h
+        self._plans = {}
+
+    @property
+    def handle(self):
+        return self._h
+
+    def vols(self, stream=None) -> "torch.Tensor":
+        out = torch.empty(self.nme, dtype=torch.float64, device=self.device)
+        _lib.check(_lib.load().sa_mesh_vols(self._h, _ptr(out), _stream_ptr(stream)))
+        return out
+
+    def plan(self, m: int = 1, row_begin: int = 0, row_end: int | None = None, stream=None) -> "Plan":
+        if row_end is None:
+            row_end = m * self.nq
+        key = (m, row_begin, row_end)
+        p = self._plans.get(key)
+        if p is None:
+            p = Plan(self, m, row_begin, row_end, stream)
+            self._plans[key] = p
+        return p
+
+    def close(self):
+        for p in self._plans.values():
+            p.close()
+        self._plans.clear()
+        if getattr(self, "_h", None):
+            _lib.load().sa_mesh_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - GC timing
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class DeviceCSR:
+    """Block CSR on the device: indptr int64 (relative), indices int32 (global
+    column dofs), vals f64; rows [row_begin, row_end) of an ncols matrix."""
+
+    row_begin: int
+    row_end: int
+    ncols: int
+    indptr: "torch.Tensor"
+    indices: "torch.Tensor"
+    vals: "torch.Tensor"
+
+    @property
+    def nnz(self) -> int:
+        return int(self.vals.numel())
+
+
+class Plan:
+    """Symbolic phase of one dof-row block (sa_plan)."""
+
+    def __init__(self, dmesh: DeviceMesh, m: int, row_begin: int, row_end: int, stream=None):
+        L = _lib.load()
+        self.dmesh = dmesh
+        self.m = m
+        self.row_begin, self.row_end = row_begin, row_end
+        h = ctypes.c_void_p()
+        with torch.cuda.device(dmesh.device):
+            _lib.check(L.sa_plan_create(dmesh.handle, m, row_begin, row_end, _stream_ptr(stream), ctypes.byref(h)))
+        self._h = h
+        nr, nnz, md = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _lib.check(L.sa_plan_info(h, ctypes.byref(nr), ctypes.byref(nnz), ctypes.byref(md)))
+        self.nrows, self.nnz, self.max_row_nodes = nr.value, nnz.value, md.value
+        self._pattern = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def pattern(self, stream=None):
+        """Structural (indptr int64 relative, indices int32) of the block."""
+        if self._pattern is None:
+            dev = self.dmesh.device
+            ip = torch.empty(self.nrows + 1, dtype=torch.int64, device=dev)
+            ix = torch.empty(max(self.nnz, 1), dtype=torch.int32, device=dev)
+            _lib.check(_lib.load().sa_plan_pattern(self._h, _ptr(ip), _ptr(ix), _stream_ptr(stream)))
+            self._pattern = (ip, ix[: self.nnz])
+        return self._pattern
+
+    def coeffs(self, kernels) -> tuple[_lib.SaCoeffs, list]:
+        """Pack the kernels' nodal coefficients into an sa_coeffs (device)."""
+        dev = self.dmesh.device
+        c = _lib.SaCoeffs()
+        c.w_const = c.lamb_const = c.mu_const = 1.0
+        keep = []
+
+        def up(a):
+            t = _to_dev(a, torch.float64, dev)
+            keep.append(t)
+            return _ptr(t)
+
+        for k in kernels:
+            if k.op == "mass":
+                if k.w is not None:
+                    c.w = up(k.w)
+                else:
+                    c.w_const = k.w_const
+            elif k.op == "elastic":
+                if k.lamb is not None:
+                    c.lamb = up(k.lamb)
+                else:
+                    c.lamb_const = k.lamb_const
+                if k.mu is not None:
+                    c.mu = up(k.mu)
+                else:
+                    c.mu_const = k.mu_const
+            elif k.op == "general":
+                d = self.dmesh.d
+                if k.A is not None:
+                    c.A = up(k.A.reshape(-1))
+                else:
+                    for i, v in enumerate(np.asarray(k.A_const, dtype=np.float64).reshape(-1)):
+                        c.A_const[i] = v
+                if k.b is not None:
+                    c.b = up(k.b.reshape(-1))
+                if k.c is not None:
+                    c.c = up(k.c.reshape(-1))
+                if k.a0 is not None:
+                    c.a0 = up(k.a0)
+                else:
+                    c.a0_const = k.a0_const
+                del d
+        return c, keep
+
+    def numeric(self, kernels, out=None, stream=None, sync: bool = True):
+        """Values of every structural entry for each kernel (ascending op-bit
+        order).  Returns (list of vals tensors, list of exact-zero counts or
+        None when sync=False)."""
+        ops = 0
+        for k in kernels:
+            ops |= OP_BITS[k.op]
+        order = sorted(kernels, key=lambda k: OP_BITS[k.op])
+        n = len(order)
+        dev = self.dmesh.device
+        if out is None:
+            out = [torch.empty(max(self.nnz, 1), dtype=torch.float64, device=dev) for _ in range(n)]
+        cf, keep = self.coeffs(order)
+        ptrs = (ctypes.c_void_p * 4)(*[o.data_ptr() for o in out] + [0] * (4 - n))
+        nz = (ctypes.c_int64 * 4)()
+        with torch.cuda.device(dev):
+            rc = _lib.load().sa_numeric(self._h, ops, ctypes.byref(cf), ptrs,
+                                        nz if sync else None, _stream_ptr(stream))
+        _lib.check(rc)
+        del keep
+        vals = [o[: self.nnz] for o in out]
+        by_kernel = {id(k): v for k, v in zip(order, vals)}
+        zeros = {id(k): int(nz[i]) for i, k in enumerate(order)} if sync else None
+        return ([by_kernel[id(k)] for k in kernels],
+                [zeros[id(k)] for k in kernels] if sync else None)
+
+    def compact(self, vals: "torch.Tensor", n_zero: int, stream=None) -> DeviceCSR:
+        """Canonical block CSR: exact-zero sums dropped (sparse.py:108-111)."""
+        ip, ix = self.pattern(stream)
+        ncols = self.m * self.dmesh.nq
+        if n_zero == 0:
+            return DeviceCSR(self.row_begin, self.row_end, ncols, ip, ix, vals)
+        dev = self.dmesh.device
+        nnz = self.nnz - n_zero
+        nip = torch.empty(self.nrows + 1, dtype=torch.int64, device=dev)
+        nix = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+        nva = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
+        _lib.check(_lib.load().sa_compact(self._h, _ptr(vals), _ptr(nip), _ptr(nix), _ptr(nva),
+                                          _stream_ptr(stream)))
+        return DeviceCSR(self.row_begin, self.row_end, ncols, nip, nix[:nnz], nva[:nnz])
+
+    def assemble(self, kernels, stream=None) -> list[DeviceCSR]:
+        vals, zeros = self.numeric(kernels, stream=stream, sync=True)
+        return [self.compact(v, z, stream) for v, z in zip(vals, zeros)]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.load().sa_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def device_volumes(q, me, core: str = "SkylakeX") -> np.ndarray:
+    """Simplex volumes computed on the B200 (numpy-det factorisation,
+    mesh.py:38-43); raises DegenerateSimplexError like compute_volumes."""
+    dm = DeviceMesh(q, me, None, core=core)
+    try:
+        return dm.vols().cpu().numpy()
+    finally:
+        dm.close()
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(_lib.load().sa_launch_count(1 if reset else 0))

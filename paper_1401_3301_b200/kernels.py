@@ -1,0 +1,129 @@
+"""Kernel descriptors with the reference constructors' signatures.
+
+Reference kernel objects (kernels.py:258-387) precompute per-element data on
+the CPU (gradients, W = w[me], lambs/mus).  These descriptors only evaluate
+the nodal coefficients (``_nodal_values``, kernels.py:268-278) and run the
+reference's argument checks; everything per element happens on the B200
+inside the numeric phase.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .errors import RangeGuardError
+
+
+def nodal_values(value, q: np.ndarray):
+    """Constant -> (None, float); callable f(q) -> ((nq,) f64, None), with the
+    reference's shape check (kernels.py:268-278)."""
+    if callable(value):
+        out = np.asarray(value(q), dtype=np.float64)
+        if out.shape != (q.shape[1],):
+            raise ValueError(f"coefficient returned shape {out.shape}, expected ({q.shape[1]},)")
+        return np.ascontiguousarray(out), None
+    if isinstance(value, np.ndarray):
+        out = np.asarray(value, dtype=np.float64)
+        if out.shape != (q.shape[1],):
+            raise ValueError(f"coefficient has shape {out.shape}, expected ({q.shape[1]},)")
+        return np.ascontiguousarray(out), None
+    return None, float(value)
+
+
+class MassKernel:
+    """Weighted mass matrix, weight interpolated at the vertices
+    (MassKernel, kernels.py:281-303)."""
+
+    symmetric = True
+    op = "mass"
+    m = 1
+
+    def __init__(self, mesh, weight=1.0):
+        self.mesh = mesh
+        self.w, self.w_const = nodal_values(weight, mesh.q)
+
+
+class StiffnessKernel:
+    """Scalar stiffness (Laplacian) matrix (StiffnessKernel, kernels.py:306-329)."""
+
+    symmetric = True
+    op = "stiffness"
+    m = 1
+
+    def __init__(self, mesh):
+        self.mesh = mesh
+
+
+class ElasticKernel:
+    """Isotropic linear elasticity, m = d unknowns per node, interleaved dofs
+    (ElasticKernel, kernels.py:332-387)."""
+
+    symmetric = True
+    op = "elastic"
+
+    def __init__(self, mesh, lamb=1.0, mu=1.0):
+        d = mesh.q.shape[0]
+        if d not in (2, 3):
+            raise ValueError(f"elastic tables are defined for d in {{2, 3}}, got {d}")
+        self.mesh = mesh
+        self.d = self.m = d
+        self.lamb, self.lamb_const = nodal_values(lamb, mesh.q)
+        self.mu, self.mu_const = nodal_values(mu, mesh.q)
+        lam_n = self.lamb if self.lamb is not None else np.full(mesh.q.shape[1], self.lamb_const)
+        mu_n = self.mu if self.mu is not None else np.full(mesh.q.shape[1], self.mu_const)
+        bad = lam_n + mu_n <= 0.0
+        if np.any(bad):
+            node = int(np.flatnonzero(bad)[0])
+            raise ValueError(f"Lame parameters must satisfy lamb + mu > 0; violated at node {node}")
+
+
+def _field(value, q, shape_tail, name):
+    """Nodal field of shape (nq, *shape_tail): constant array of shape
+    shape_tail, callable f(q) -> (*shape_tail, nq) like the reference
+    coefficient convention, or an explicit (nq, *shape_tail) array."""
+    nq = q.shape[1]
+    if value is None:
+        return None, np.zeros(shape_tail)
+    if callable(value):
+        out = np.asarray(value(q), dtype=np.float64)
+        if out.shape != tuple(shape_tail) + (nq,):
+            raise ValueError(f"{name} returned shape {out.shape}, expected {tuple(shape_tail) + (nq,)}")
+        return np.ascontiguousarray(np.moveaxis(out, -1, 0)), None
+    arr = np.asarray(value, dtype=np.float64)
+    if arr.shape == tuple(shape_tail) or (arr.ndim == 0 and not shape_tail):
+        return None, arr.reshape(shape_tail)
+    if arr.shape == (nq,) + tuple(shape_tail):
+        return np.ascontiguousarray(arr), None
+    raise ValueError(f"{name} has shape {arr.shape}; expected {tuple(shape_tail)} or {(nq,) + tuple(shape_tail)}")
+
+
+class GeneralKernel:
+    """General second-order operator -div(A grad u) + div(b u) + c.grad u + a0 u
+    (weak form and quadrature in DESIGN.md 3.4).  Row = test
+    function, as in the reference.  Not symmetric in general.
+
+    A: (d, d) constant, (nq, d, d) nodal array or callable q -> (d, d, nq);
+    b, c: (d,) constant, (nq, d) nodal or callable q -> (d, nq); a0: scalar,
+    (nq,) nodal or callable q -> (nq,).  Missing terms are zero."""
+
+    op = "general"
+    m = 1
+
+    def __init__(self, mesh, A=None, b=None, c=None, a0=None):
+        q = mesh.q
+        d = q.shape[0]
+        if d not in (1, 2, 3):
+            raise RangeGuardError(f"dimension must be 1, 2 or 3, got {d}")
+        self.mesh = mesh
+        self.A, self.A_const = _field(A, q, (d, d), "A")
+        self.b, b_const = _field(b, q, (d,), "b")
+        self.c, c_const = _field(c, q, (d,), "c")
+        if self.b is None and np.any(b_const != 0):
+            self.b = np.ascontiguousarray(np.broadcast_to(b_const, (q.shape[1], d)))
+        if self.c is None and np.any(c_const != 0):
+            self.c = np.ascontiguousarray(np.broadcast_to(c_const, (q.shape[1], d)))
+        if a0 is None:
+            self.a0, self.a0_const = None, 0.0
+        else:
+            self.a0, self.a0_const = nodal_values(a0, q)
+        self.symmetric = False

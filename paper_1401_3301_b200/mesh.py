@@ -1,0 +1,110 @@
+"""Simplicial meshes: the input side of the assembly path.
+
+``Mesh`` mirrors the reference type (mesh.py:46-101): ``q`` (d, nq) f64,
+``me`` (d+1, nme) int64, ``vols`` (nme,) f64, immutable.  The drivers accept
+any object with those three attributes, in particular the reference's own
+``simplex_asm.Mesh``.
+
+``generate_hypercube_mesh`` restates the reference's Kuhn generator
+(mesh.py:104-140) and ``jittered_hypercube_mesh`` adds the seeded interior
+jitter of SURVEY.md 8(d) used for every benchmark configuration.
+"""
+
+from __future__ import annotations
+
+import itertools
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import CapacityError
+
+_MAX_INDEX = np.iinfo(np.int64).max
+
+
+@dataclass(frozen=True, eq=False)
+class Mesh:
+    q: np.ndarray     # (d, nq) vertex coordinates
+    me: np.ndarray    # (d+1, nme) zero-based connectivity
+    vols: np.ndarray  # (nme,) simplex volumes
+
+    @classmethod
+    def from_arrays(cls, q, me, vols=None) -> "Mesh":
+        """Cast like the reference (mesh.py:54-58).  Volumes, when not given,
+        are computed on the B200 from the numpy-det factorisation
+        (``device.device_volumes``); the reference computes them with numpy
+        on the host, which agrees to a few ulp."""
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        me = np.ascontiguousarray(me, dtype=np.int64)
+        if vols is None:
+            from .device import device_volumes
+
+            vols = device_volumes(q, me)
+        return cls(q, me, np.ascontiguousarray(vols, dtype=np.float64))
+
+    @property
+    def d(self) -> int:
+        return self.q.shape[0]
+
+    @property
+    def nq(self) -> int:
+        return self.q.shape[1]
+
+    @property
+    def nme(self) -> int:
+        return self.me.shape[1]
+
+
+def hypercube_arrays(d: int, n: int):
+    """(q, me) of the Kuhn triangulation of [0,1]^d with n cells per axis:
+    row-major grid points, d! simplices per cell (one per axis permutation),
+    the simplices of a cell adjacent (mesh.py:104-140)."""
+    if d < 1:
+        raise ValueError(f"dimension must be >= 1, got {d}")
+    if n < 1:
+        raise ValueError(f"subdivision count must be >= 1, got {n}")
+    nq = (n + 1) ** d
+    nme = math.factorial(d) * n ** d
+    if nq > _MAX_INDEX or (d + 1) * nme > _MAX_INDEX:
+        raise CapacityError(f"hypercube mesh d={d}, n={n} exceeds the platform index range")
+    grid = np.indices((n + 1,) * d).reshape(d, -1)
+    q = grid / float(n)
+    strides = (n + 1) ** np.arange(d - 1, -1, -1, dtype=np.int64)
+    cells = np.indices((n,) * d, dtype=np.int64).reshape(d, -1)
+    base = strides @ cells
+    me = np.empty((nme, d + 1), dtype=np.int64)
+    for p, perm in enumerate(itertools.permutations(range(d))):
+        rows = me[p::math.factorial(d)]
+        rows[:, 0] = base
+        acc = base.copy()
+        for j, axis in enumerate(perm):
+            acc = acc + strides[axis]
+            rows[:, j + 1] = acc
+    return q, np.ascontiguousarray(me.T)
+
+
+def jitter_interior(q: np.ndarray, n: int, amplitude: float, seed: int) -> np.ndarray:
+    """interior nodes (all coordinates strictly inside (0,1))
+    move by rng.uniform(-a*h, a*h) per coordinate, h = 1/n."""
+    q = q.copy()
+    h = 1.0 / n
+    interior = np.all((q > 0) & (q < 1), axis=0)
+    rng = np.random.default_rng(seed)
+    q[:, interior] += rng.uniform(-amplitude * h, amplitude * h, size=(q.shape[0], int(interior.sum())))
+    return q
+
+
+def generate_hypercube_mesh(d: int, n: int, vols=None) -> Mesh:
+    q, me = hypercube_arrays(d, n)
+    return Mesh.from_arrays(q, me, vols)
+
+
+def jittered_hypercube_mesh(d: int, n: int, seed: int, amplitude: float | None = None, vols=None) -> Mesh:
+    """The benchmark meshes: Kuhn cube + seeded interior jitter
+    (a = 0.2 in 2D, 0.15 in 3D unless given)."""
+    if amplitude is None:
+        amplitude = 0.2 if d <= 2 else 0.15
+    q, me = hypercube_arrays(d, n)
+    q = jitter_interior(q, n, amplitude, seed)
+    return Mesh.from_arrays(q, me, vols)

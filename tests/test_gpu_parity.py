@@ -1,0 +1,171 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+golden fixtures and the CPU oracle.  Bar: bit-exact CSR pattern and -- since
+every entry is folded in ascending element order with bit-exact element
+values -- bit-exact values too (north_star's tolerance, 1e-12 of the row max,
+is asserted as well so a failure says which bar broke)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_1401_3301_b200 as P
+from conftest import device_kernel_for, golden_cases, load_golden, oracle_op_for
+
+pytestmark = pytest.mark.gpu
+
+VAL_RTOL = 1e-12  # north_star: fp64 values within 1e-12 relative to each row's max magnitude
+
+
+def assert_csr_equal(got, rp, ci, va, bitwise=True):
+    assert np.array_equal(got.row_ptr, rp), "row_ptr differs"
+    assert np.array_equal(got.col_idx, ci), "col_idx differs"
+    rows = np.repeat(np.arange(len(rp) - 1), np.diff(rp))
+    rowmax = np.zeros(len(rp) - 1)
+    np.maximum.at(rowmax, rows, np.abs(va))
+    err = np.abs(got.vals - va)
+    assert np.all(err <= VAL_RTOL * rowmax[rows]), f"max rel err {np.max(err / np.maximum(rowmax[rows], 1e-300))}"
+    if bitwise:
+        assert np.array_equal(got.vals, va), f"{np.count_nonzero(got.vals != va)} values not bitwise"
+
+
+def golden_mesh(g):
+    return P.Mesh(g["q"], g["me"], g["vols"])
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_golden_bitwise(cuda_ok, name):
+    g = load_golden(name)
+    mesh = golden_mesh(g)
+    k = device_kernel_for(name, g, mesh)
+    got = P.assemble_vector_b200(mesh, k) if k.m > 1 else P.assemble_b200(mesh, k)
+    assert got.shape == tuple(g["shape"])
+    assert_csr_equal(got, g["row_ptr"], g["col_idx"], g["vals"])
+
+
+def _jittered(d, n, seed):
+    from oracle import oracle as O
+
+    q, me = P.hypercube_arrays(d, n)
+    q = P.jitter_interior(q, n, 0.2 if d == 2 else 0.15, seed)
+    return P.Mesh(q, me, O.volumes(q, me))
+
+
+def _oracle(mesh, kind, nthreads=16, **kw):
+    from oracle import oracle as O
+
+    op = O.OracleOp(kind, mesh.q.shape[0], mesh.vols, **kw)
+    return O.assemble(mesh.q, mesh.me, op, nthreads=nthreads)
+
+
+@pytest.mark.parametrize("d,n", [(2, 200), (3, 40)])
+def test_fused_mass_stiffness_vs_oracle(cuda_ok, d, n):
+    # C1 is d=2, n=200 (configs[0]); fused numeric pass, two outputs
+    mesh = _jittered(d, n, 14013301)
+    mass, stiff = P.assemble_many_b200(mesh, [P.MassKernel(mesh), P.StiffnessKernel(mesh)])
+    assert_csr_equal(mass, *_oracle(mesh, "mass", w=np.ones(mesh.q.shape[1])))
+    assert_csr_equal(stiff, *_oracle(mesh, "stiffness"))
+
+
+def test_elastic_vs_oracle(cuda_ok):
+    mesh = _jittered(3, 16, 14013304)
+    lam = 1.0 + mesh.q[0]
+    mu = 0.5 + mesh.q[2] ** 2
+    got = P.assemble_vector_b200(mesh, P.ElasticKernel(mesh, lam, mu))
+    assert_csr_equal(got, *_oracle(mesh, "elastic", lamb=lam, mu=mu))
+
+
+def test_general_vs_oracle(cuda_ok):
+    mesh = _jittered(3, 20, 14013305)
+    nq = mesh.q.shape[1]
+    rng = np.random.default_rng(14013305)
+    R = rng.standard_normal((nq, 3, 3))
+    A = np.eye(3)[None] + 0.5 * np.einsum("nij,nkj->nik", R, R) / 3.0
+    b, c, a0 = rng.standard_normal((nq, 3)), rng.standard_normal((nq, 3)), rng.uniform(0, 1, nq)
+    got = P.assemble_b200(mesh, P.GeneralKernel(mesh, A=A, b=b, c=c, a0=a0))
+    assert_csr_equal(got, *_oracle(mesh, "general", A=A, b=b, c=c, a0=a0))
+
+
+def test_general_reduces_to_stiffness_and_mass(cuda_ok):
+    mesh = _jittered(3, 10, 3)
+    st = P.assemble_b200(mesh, P.StiffnessKernel(mesh))
+    g = P.assemble_b200(mesh, P.GeneralKernel(mesh, A=np.eye(3)))
+    assert_csr_equal(g, st.row_ptr, st.col_idx, st.vals)  # d=3: (4a)(v/4) == a*v exactly
+    w = 1.0 + mesh.q[1]
+    m = P.assemble_b200(mesh, P.MassKernel(mesh, w))
+    g2 = P.assemble_b200(mesh, P.GeneralKernel(mesh, a0=w))
+    assert_csr_equal(g2, m.row_ptr, m.col_idx, m.vals)
+
+
+def test_row_blocks_stitch_bitwise(cuda_ok):
+    from paper_1401_3301_b200 import parallel
+    from paper_1401_3301_b200.device import DeviceMesh
+
+    mesh = _jittered(3, 18, 9)
+    full = P.assemble_b200(mesh, P.StiffnessKernel(mesh))
+    dm = DeviceMesh(mesh.q, mesh.me, mesh.vols)
+    blocks = []
+    for rb, re_ in parallel.row_blocks(mesh.q.shape[1], 1, 3):
+        (csr,) = dm.plan(1, rb, re_).assemble([P.StiffnessKernel(mesh)])
+        blocks.append((rb, re_, csr.indptr.cpu().numpy(), csr.indices.cpu().numpy(), csr.vals.cpu().numpy()))
+    rp, ci, va = parallel.stitch(blocks, mesh.q.shape[1], mesh.q.shape[1])
+    assert_csr_equal(full, rp, ci, va)
+
+
+def test_deterministic_run_to_run(cuda_ok):
+    from paper_1401_3301_b200.device import DeviceMesh
+
+    mesh = _jittered(2, 300, 1)
+    dm = DeviceMesh(mesh.q, mesh.me, mesh.vols)
+    plan = dm.plan(1)
+    ks = [P.MassKernel(mesh), P.StiffnessKernel(mesh)]
+    h = set()
+    for _ in range(3):
+        vals, _z = plan.numeric(ks)
+        h.add(tuple(hashlib.sha256(v.cpu().numpy().tobytes()).hexdigest() for v in vals))
+    assert len(h) == 1
+
+
+def test_degenerate_element_named(cuda_ok):
+    q = np.array([[0.0, 1.0, 2.0, 0.0], [0.0, 1.0, 2.0, 1.0]])
+    me = np.array([[0, 0], [3, 1], [1, 2]])
+    mesh = P.Mesh(q, me, np.array([0.5, 0.0]))
+    with pytest.raises(P.DegenerateSimplexError) as ei:
+        P.assemble_b200(mesh, P.StiffnessKernel(mesh))
+    assert ei.value.element == 1
+    with pytest.raises(P.DegenerateSimplexError) as ei:
+        P.Mesh.from_arrays(q, me)
+    assert ei.value.element == 1
+
+
+def test_index_range_error(cuda_ok):
+    q, me = P.hypercube_arrays(2, 2)
+    me = me.copy()
+    me[2, 5] = q.shape[1]
+    mesh = P.Mesh(q, me, np.full(me.shape[1], 0.125))
+    with pytest.raises(P.IndexRangeError, match=r"me\[2, 5\]"):
+        P.assemble_b200(mesh, P.StiffnessKernel(mesh))
+
+
+def test_device_volumes_close_to_numpy_det(cuda_ok):
+    from oracle import oracle as O
+
+    for d, n in [(1, 50), (2, 60), (3, 12)]:
+        q, me = P.hypercube_arrays(d, n)
+        q = P.jitter_interior(q, n, 0.15, 2)
+        v = P.device_volumes(q, me)
+        ref = O.volumes(q, me)
+        assert np.max(np.abs(v - ref) / ref) < 1e-14
+
+
+def test_full_size_c2_properties(cuda_ok):
+    """configs[1] (2D N=2000, 8M triangles) at full size: pattern and values
+    vs the threaded oracle, plus size-independent invariants."""
+    mesh = _jittered(2, 2000, 14013302)
+    mass, stiff = P.assemble_many_b200(mesh, [P.MassKernel(mesh), P.StiffnessKernel(mesh)])
+    assert_csr_equal(stiff, *_oracle(mesh, "stiffness"))
+    assert_csr_equal(mass, *_oracle(mesh, "mass", w=np.ones(mesh.q.shape[1])))
+    assert abs(mass.vals.sum() - 1.0) < 1e-12           # total mass = |domain|
+    rows = np.repeat(np.arange(stiff.nrows), np.diff(stiff.row_ptr))
+    rs = np.bincount(rows, weights=stiff.vals, minlength=stiff.nrows)
+    assert np.max(np.abs(rs)) < 1e-9                    # constants are in the kernel

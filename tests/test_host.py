@@ -1,0 +1,100 @@
+"""Host-side logic and the C-ABI library surface (no GPU needed)."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1401_3301_b200 as P
+from conftest import ROOT, golden_cases, load_golden
+from paper_1401_3301_b200 import _build, _lib, parallel
+
+
+def test_library_exports_every_header_symbol():
+    path = _build.build()
+    L = ctypes.CDLL(path)
+    header = open(os.path.join(ROOT, "include", "simplex_asm_b200.h")).read()
+    declared = set(re.findall(r"^\s*(?:int|int64_t|const char \*)\s*(sa_\w+)\(", header, re.M))
+    assert declared == set(_lib.EXPORTS)
+    for name in declared:
+        assert hasattr(L, name), name
+
+
+def test_library_is_sm100a():
+    out = os.popen(f"cuobjdump --list-elf {_build.build()} 2>&1").read()
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("d,n", [(1, 7), (2, 5), (3, 3), (3, 4)])
+def test_hypercube_matches_reference_generator(d, n):
+    # golden fixtures hold the reference generator's output (mesh.py:104-140)
+    name = f"stiff_d{d}_n{n}_kuhn"
+    q, me = P.hypercube_arrays(d, n)
+    if name in golden_cases():
+        g = load_golden(name)
+        assert np.array_equal(q, g["q"]) and np.array_equal(me, g["me"])
+    assert me.shape == (d + 1, int(np.prod(range(1, d + 1))) * n ** d)
+    assert q.shape == (d, (n + 1) ** d)
+
+
+@pytest.mark.parametrize("name", golden_cases("stiff_"))
+def test_generator_and_jitter_reproduce_golden_meshes(name):
+    g = load_golden(name)
+    d = g["q"].shape[0]
+    n = int(name.split("_n")[1].split("_")[0])
+    q, me = P.hypercube_arrays(d, n)
+    assert np.array_equal(me, g["me"])
+    if name.endswith("_jit"):
+        seed = {(1, 40): 5, (2, 15): 11, (3, 6): 13, (3, 8): 14}[(d, n)]
+        q = P.jitter_interior(q, n, 0.2 if d < 3 else 0.15, seed)
+    assert np.array_equal(q, g["q"])
+
+
+def test_row_blocks_cover_and_align():
+    for nq, m, p in [(10, 1, 3), (11, 3, 4), (1000, 2, 8), (5, 1, 8)]:
+        bl = parallel.row_blocks(nq, m, p)
+        assert bl[0][0] == 0 and bl[-1][1] == m * nq
+        for (a, b), (c, _) in zip(bl[:-1], bl[1:]):
+            assert b == c and a % m == 0 and b % m == 0
+
+
+def test_stitch_roundtrip():
+    rng = np.random.default_rng(0)
+    nrows = 9
+    lens = rng.integers(0, 4, nrows)
+    rp = np.concatenate([[0], np.cumsum(lens)])
+    ci = rng.integers(0, 9, rp[-1])
+    va = rng.standard_normal(rp[-1])
+    blocks = []
+    for rb, re_ in [(0, 4), (4, 5), (5, 9)]:
+        s, e = rp[rb], rp[re_]
+        blocks.append((rb, re_, rp[rb:re_ + 1] - s, ci[s:e], va[s:e]))
+    r2, c2, v2 = parallel.stitch(blocks, nrows, 9)
+    assert np.array_equal(r2, rp) and np.array_equal(c2, ci) and np.array_equal(v2, va)
+
+
+def test_kernel_descriptor_checks():
+    q, me = P.hypercube_arrays(2, 3)
+    mesh = P.Mesh(q, me, np.full(me.shape[1], 1.0 / 18))
+    with pytest.raises(ValueError, match="shape"):
+        P.MassKernel(mesh, lambda q: np.ones(3))
+    with pytest.raises(ValueError, match="lamb \\+ mu > 0"):
+        P.ElasticKernel(mesh, 1.0, -2.0)
+    with pytest.raises(ValueError):
+        P.ElasticKernel(P.Mesh(np.zeros((1, 2)), np.array([[0], [1]]), np.ones(1)))
+    k = P.MassKernel(mesh, 2.5)
+    assert k.w is None and k.w_const == 2.5
+    g = P.GeneralKernel(mesh, A=np.eye(2), b=[1.0, 0.0], a0=lambda q: q[0])
+    assert g.A is None and g.b.shape == (q.shape[1], 2) and g.c is None and g.a0.shape == (q.shape[1],)
+    assert not g.symmetric
+
+
+def test_error_mapping():
+    from paper_1401_3301_b200.errors import CapacityError
+
+    with pytest.raises(ValueError):
+        _lib.check(_lib.SA_ERR_ARG)
+    with pytest.raises(CapacityError):
+        _lib.check(_lib.SA_ERR_CAPACITY)
