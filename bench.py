@@ -326,7 +326,7 @@ def main():
         "numeric_ms": ms_per_step,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                     "algorithmic_bytes": b_num, "kernel": "k_numeric_rowgather",
+                     "algorithmic_bytes": b_num, "kernel": "k_numeric_tile",
                      "frac_of_8TBps_nominal": achieved / 8000.0},
         "gpu_launches": launches,
         "clocks": clk.summary(),

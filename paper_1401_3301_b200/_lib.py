@@ -24,7 +24,7 @@ SA_CORE = {"SkylakeX": 0, "Haswell": 1}
 # every symbol include/simplex_asm_b200.h declares
 EXPORTS = (
     "sa_mesh_create", "sa_mesh_vols", "sa_mesh_destroy",
-    "sa_plan_create", "sa_plan_info", "sa_plan_pattern", "sa_plan_destroy",
+    "sa_plan_create", "sa_plan_info", "sa_plan_stats", "sa_plan_pattern", "sa_plan_destroy",
     "sa_numeric", "sa_compact",
     "sa_last_error", "sa_bad_index", "sa_launch_count",
 )
@@ -69,6 +69,7 @@ def load(build_if_missing: bool = True):
     L.sa_mesh_destroy.argtypes = [vp]
     L.sa_plan_create.argtypes = [vp, ctypes.c_int, i64, i64, vp, ctypes.POINTER(vp)]
     L.sa_plan_info.argtypes = [vp, i64p, i64p, i64p]
+    L.sa_plan_stats.argtypes = [vp, i64p, ctypes.c_int]
     L.sa_plan_pattern.argtypes = [vp, vp, vp, vp]
     L.sa_plan_destroy.argtypes = [vp]
     L.sa_numeric.argtypes = [vp, ctypes.c_int, ctypes.POINTER(SaCoeffs), ctypes.POINTER(vp), i64p, vp]

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <unordered_map>
 #include <vector>
 
 #include "sa_common.cuh"
@@ -46,6 +47,42 @@ struct sa_plan {
     int32_t *indices = nullptr;   // (nnz) global column dofs
     int64_t *counters = nullptr;  // [0..3] zero counts per output, [4] bad element, [5] capacity flag
     int64_t *scan_tmp = nullptr;
+    // block numeric kernel: compact incidences + fold program
+    uint32_t *inc_e = nullptr;    // (n_inc) e | alpha<<30
+    uint16_t *fold = nullptr;     // ((d+1) n_inc) per slot: u | beta<<6 | last<<8
+    bool fold_ok = false;         // every node has <= 64 incidences
+    // fold templates (tile kernel)
+    bool tm_ok = false;
+    int64_t n_templates = 0, tm_nwords = 0;
+    int tile_rows = 0;
+    uint32_t *tile_e0 = nullptr, *tile_tm = nullptr, *tm_off = nullptr, *tm = nullptr;
+    // per tile size R = 2^c (c = 0..5): max incidences / node-level entries in one tile of R rows
+    int64_t tile_max_inc[6] = {0, 0, 0, 0, 0, 0};
+    int64_t tile_max_ent[6] = {0, 0, 0, 0, 0, 0};
+};
+
+// numeric-phase arguments (shared by the per-dimension translation units)
+struct NumArgs {
+    const void *qv;
+    const void *me;
+    const double *vols;
+    int64_t nnodes;
+    int64_t node_begin;
+    const int64_t *inc_ptr;
+    const uint2 *inc;
+    const int64_t *colptr;
+    const int64_t *indptr;
+    int acc_stride;  // smem accumulator rows per output (m*m*max_deg)
+    double *vals[2];
+    int64_t *counters;
+    // coefficients
+    const double *w; double w_const;
+    const double *lamb; double lamb_const;
+    const double *mu; double mu_const;
+    const double *A; const double *b; const double *c; const double *a0;
+    double A_const[9]; double a0_const;
+    double mass_coef_diag, mass_coef_off;  // 2/((d+1)(d+2)(d+3)), 1/(...) as Python computes them
+    double mass_wc;  // constant weight: (wsum + w) + w, the same for every (alpha, beta)
 };
 
 namespace {
@@ -220,6 +257,167 @@ __global__ void k_inc_ranks(const typename IdxT<D>::type *__restrict__ me, const
     }
 }
 
+// Fold program of node row nl: for each column k (ascending), the
+// contributing (incidence u, local vertex beta) pairs in ascending element
+// order, as u | beta << 6; the last pair of each column has bit 8 set.
+template <int D>
+__global__ void k_fold_lists(const int64_t *__restrict__ inc_ptr, const uint2 *__restrict__ inc, int64_t nnodes,
+                             const int64_t *__restrict__ colptr, uint32_t *__restrict__ inc_e,
+                             uint16_t *__restrict__ fold, unsigned long long *too_many)
+{
+    int64_t nl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (nl >= nnodes) return;
+    const int64_t t0 = inc_ptr[nl];
+    const int ni = (int)(inc_ptr[nl + 1] - t0);
+    for (int u = 0; u < ni; ++u) inc_e[t0 + u] = inc[t0 + u].x;
+    if (ni > 64) { atomicOr(too_many, 1ull); return; }
+    const int deg = (int)(colptr[nl + 1] - colptr[nl]);
+    uint16_t *out = fold + (int64_t)(D + 1) * t0;
+    int w = 0;
+    for (int k = 0; k < deg; ++k) {
+        int last = -1;
+        for (int u = 0; u < ni; ++u) {
+            const unsigned r = inc[t0 + u].y;
+            for (int b = 0; b <= D; ++b)
+                if ((int)((r >> (8 * b)) & 0xff) == k) { out[w] = (uint16_t)(u | (b << 6)); last = w; ++w; }
+        }
+        if (last >= 0) out[last] |= 256;
+    }
+}
+
+// ---- tile templates -------------------------------------------------------
+// A tile is R consecutive node rows, processed by one warp.  Its template
+// (relative to the tile's smallest element id e_base) holds
+//   w[0] = n_elem | nrows << 8 | nslots << 16,  w[1] = NE node-level entries
+//   w[2 .. 2+ne)            de[j]: the tile's distinct elements, ascending
+//   w[2+ne .. 2+2ne)        per element: 4 x 8-bit slot id of local row
+//                           alpha = 0..3 (0xff: vertex not in the tile)
+//   w[2+2ne .. 2+2ne+2NI)   per slot (= incidence, row-major, ascending
+//                           element per row): 4 x 16-bit fold positions,
+//                           one per local column beta
+//   w[PB .. PB+nrows)       per row: deg | entb << 16
+//   w[OB .. )               NE+1 uint16 entry offsets into the fold array
+// The fold array of a tile is entry-major: entry k's contributions occupy
+// [off[k], off[k+1]) in ascending element order.  Element lanes scatter their
+// local rows straight into it; row lanes then sum contiguous runs.
+// Tiles with equal templates share one copy: all interior tiles of a
+// structured mesh collapse to a few dozen.
+__device__ __forceinline__ uint64_t fnv_step(uint64_t h, uint32_t x)
+{
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { h ^= (x >> (8 * i)) & 0xff; h *= 1099511628211ull; }
+    return h;
+}
+
+constexpr int TILE_MAX_ELEM = 255;
+
+__host__ __device__ inline int64_t tile_stride_bound(int64_t NI, int64_t NE, int64_t R)
+{
+    return 2 + 2 * (NI < TILE_MAX_ELEM ? NI : TILE_MAX_ELEM) + 2 * NI + R + (NE + 2) / 2 + 4;
+}
+
+template <int D>
+__global__ void k_tile_build(const int64_t *__restrict__ inc_ptr, const uint32_t *__restrict__ inc_e,
+                             const uint16_t *__restrict__ fold, const int64_t *__restrict__ colptr, int64_t nnodes,
+                             int R, int64_t ntiles, int stride, uint32_t *__restrict__ scratch,
+                             uint32_t *__restrict__ words_out, uint64_t *__restrict__ sig,
+                             uint32_t *__restrict__ tile_e0, unsigned long long *fail)
+{
+    const int64_t T = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (T >= ntiles) return;
+    const int64_t r0 = T * R;
+    const int nr = (int)min((int64_t)R, nnodes - r0);
+    uint32_t *w = scratch + T * (int64_t)stride;
+    const int64_t t0 = inc_ptr[r0];
+    const int NI = (int)(inc_ptr[r0 + nr] - t0);
+    const int64_t c0 = colptr[r0];
+    const int NE = (int)(colptr[r0 + nr] - c0);
+    uint32_t el[TILE_MAX_ELEM];
+    int ne = 0;
+    bool bad = NI > 254 || (D + 1) * NI > 65535 || NE > 65534;
+    for (int i = 0; i < NI && !bad; ++i) {
+        const uint32_t e = inc_e[t0 + i] & 0x3fffffffu;
+        int lo = 0, hi = ne;
+        while (lo < hi) { int mid = (lo + hi) >> 1; if (el[mid] < e) lo = mid + 1; else hi = mid; }
+        if (lo < ne && el[lo] == e) continue;
+        if (ne == TILE_MAX_ELEM) { bad = true; break; }
+        for (int k = ne; k > lo; --k) el[k] = el[k - 1];
+        el[lo] = e;
+        ++ne;
+    }
+    if (bad) { atomicOr(fail, 1ull); words_out[T] = 0; return; }
+    const uint32_t eb = ne ? el[0] : 0u;
+    tile_e0[T] = eb;
+    w[0] = (uint32_t)ne | ((uint32_t)nr << 8) | ((uint32_t)NI << 16);
+    w[1] = (uint32_t)NE;
+    for (int j = 0; j < ne; ++j) { w[2 + j] = el[j] - eb; w[2 + ne + j] = 0xffffffffu; }
+    for (int i = 0; i < NI; ++i) {
+        const uint32_t r = inc_e[t0 + i];
+        const uint32_t e = r & 0x3fffffffu, alpha = r >> 30;
+        int lo = 0, hi = ne;
+        while (lo < hi) { int mid = (lo + hi) >> 1; if (el[mid] < e) lo = mid + 1; else hi = mid; }
+        uint32_t &sw = w[2 + ne + lo];
+        sw = (sw & ~(0xffu << (8 * alpha))) | ((uint32_t)i << (8 * alpha));
+    }
+    const uint32_t SB = 2 + 2 * ne, PB = SB + 2 * NI, OB = PB + nr;
+    const uint32_t end = OB + ((NE + 2) >> 1);
+    for (uint32_t x = SB; x < end; ++x) w[x] = 0;
+    for (int row = 0; row < nr; ++row) {
+        const int64_t ip = inc_ptr[r0 + row];
+        const int ni = (int)(inc_ptr[r0 + row + 1] - ip);
+        const int deg = (int)(colptr[r0 + row + 1] - colptr[r0 + row]);
+        const int incb = (int)(ip - t0);
+        const int entb = (int)(colptr[r0 + row] - c0);
+        w[PB + row] = (uint32_t)deg | ((uint32_t)entb << 16);
+        int k = 0;
+        for (int s = 0; s < (D + 1) * ni; ++s) {
+            const uint16_t f = fold[(D + 1) * ip + s];
+            const uint32_t slot = incb + (f & 63), beta = (f >> 6) & 3;
+            const uint32_t pos = (uint32_t)((D + 1) * incb + s);
+            w[SB + 2 * slot + (beta >> 1)] |= pos << (16 * (beta & 1));
+            if (f & 256) {
+                ++k;
+                const uint32_t kg = entb + k;
+                w[OB + (kg >> 1)] |= (pos + 1) << (16 * (kg & 1));
+            }
+        }
+    }
+    words_out[T] = end;
+    uint64_t h = 1469598103934665603ull;
+    for (uint32_t x = 0; x < end; ++x) h = fnv_step(h, w[x]);
+    sig[T] = h;
+}
+
+__global__ void k_tile_pack(const int64_t *__restrict__ rep, int64_t ntm, const uint32_t *__restrict__ scratch,
+                            int stride, const uint32_t *__restrict__ words, const uint32_t *__restrict__ tm_off,
+                            uint32_t *__restrict__ tm)
+{
+    // one warp per template
+    const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= ntm) return;
+    const uint32_t *src = scratch + rep[t] * (int64_t)stride;
+    uint32_t *dst = tm + tm_off[t];
+    const uint32_t n = words[rep[t]];
+    for (uint32_t i = lane; i < n; i += 32) dst[i] = src[i];
+}
+
+__global__ void k_tile_verify(const uint32_t *__restrict__ scratch, int stride, const uint32_t *__restrict__ words,
+                              int64_t ntiles, const uint32_t *__restrict__ tile_tm,
+                              const uint32_t *__restrict__ tm_off, const uint32_t *__restrict__ tm,
+                              unsigned long long *bad)
+{
+    const int64_t T = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (T >= ntiles) return;
+    const uint32_t *a = scratch + T * (int64_t)stride;
+    const uint32_t *b = tm + tm_off[tile_tm[T]];
+    const uint32_t n = words[T];
+    bool ok = true;
+    for (uint32_t i = lane; i < n; i += 32) ok &= (a[i] == b[i]);
+    if (!__all_sync(0xffffffffu, ok) && lane == 0) atomicOr(bad, 1ull);
+}
+
 // dof-level CSR of the block: row m*nl+l has columns m*cols[k]+n
 __global__ void k_dof_csr(const int64_t *__restrict__ colptr, const int32_t *__restrict__ cols, int64_t nnodes,
                           int m, int64_t *__restrict__ indptr, int32_t *__restrict__ indices)
@@ -240,27 +438,7 @@ __global__ void k_dof_csr(const int64_t *__restrict__ colptr, const int32_t *__r
 // ---------------------------------------------------------------------------
 // numeric phase
 
-struct NumArgs {
-    const void *qv;
-    const void *me;
-    const double *vols;
-    int64_t nnodes;
-    int64_t node_begin;
-    const int64_t *inc_ptr;
-    const uint2 *inc;
-    const int64_t *colptr;
-    const int64_t *indptr;
-    int acc_stride;  // smem accumulator rows per output (m*m*max_deg)
-    double *vals[2];
-    int64_t *counters;
-    // coefficients
-    const double *w; double w_const;
-    const double *lamb; double lamb_const;
-    const double *mu; double mu_const;
-    const double *A; const double *b; const double *c; const double *a0;
-    double A_const[9]; double a0_const;
-    double mass_coef_diag, mass_coef_off;  // 2/((d+1)(d+2)(d+3)), 1/(...) as Python computes them
-};
+
 
 template <int OPS>
 __host__ __device__ constexpr int n_outputs()
@@ -275,137 +453,189 @@ __device__ __forceinline__ double nodal(const double *p, double cst, int v)
     return p ? __ldg(p + v) : cst;
 }
 
-// Fold element e's row(s) for local vertex alpha into the accumulators.
-template <int D, int M, int OPS, int CORE>
-__device__ __forceinline__ void fold_incidence(const NumArgs &a, uint2 rec, double *acc, int tid, int nthr,
-                                               bool &degenerate)
-{
-    constexpr int NOUT = n_outputs<OPS>();
-    const int64_t e = rec.x & 0x3fffffffu;
-    const int alpha = rec.x >> 30;
-    const unsigned ranks = rec.y;
+// Per-element state shared by the rows a tile needs from that element.
+template <int D>
+struct ElemGeo {
     int v[D + 1];
-    load_element<D>((const typename IdxT<D>::type *)a.me, e, v);
-    const double vol = __ldg(a.vols + e);
-    double x[D + 1][D];
+    double vol;
     double G[D + 1][D];
+    double W[D + 1], wsum;                      // mass
+    double lambs, mus;                          // elastic
+    double As[D][D], bs[D], cs[D], a0s;         // general
+    double bv[D + 1][D], cv[D + 1][D], a0v[D + 1];
+};
+
+// Raw per-element inputs, loaded in two stages (connectivity + volume, then
+// vertices + nodal coefficients) so a lane can keep two elements' loads in
+// flight before it computes either.
+template <int D>
+struct ElemRaw {
+    int v[D + 1];
+    double vol;
+    double x[D + 1][D];
+    double W[D + 1], lam[D + 1], mu[D + 1];
+    double A[D + 1][D][D], b[D + 1][D], c[D + 1][D], a0[D + 1];
+};
+
+template <int D, int OPS>
+__device__ __forceinline__ void element_load1(const NumArgs &a, int64_t e, ElemRaw<D> &r)
+{
+    load_element<D>((const typename IdxT<D>::type *)a.me, e, r.v);
+    r.vol = __ldg(a.vols + e);
+}
+
+template <int D, int OPS>
+__device__ __forceinline__ void element_load2(const NumArgs &a, ElemRaw<D> &r)
+{
     if constexpr ((OPS & (OP_STIFF | OP_ELASTIC | OP_GENERAL)) != 0) {
 #pragma unroll
-        for (int g = 0; g <= D; ++g) load_vertex<D>((const typename VecT<D>::type *)a.qv, v[g], x[g]);
-        degenerate |= element_gradients<D, CORE>(x, G);
+        for (int k = 0; k <= D; ++k) load_vertex<D>((const typename VecT<D>::type *)a.qv, r.v[k], r.x[k]);
     }
-    double ga[D];
-    if constexpr ((OPS & (OP_STIFF | OP_ELASTIC | OP_GENERAL)) != 0) select_row<D>(G, alpha, ga);
+#pragma unroll
+    for (int k = 0; k <= D; ++k) {
+        const int vk = r.v[k];
+        if constexpr ((OPS & OP_MASS) != 0) r.W[k] = a.w ? __ldg(a.w + vk) : 0.0;
+        if constexpr ((OPS & OP_ELASTIC) != 0) {
+            r.lam[k] = nodal<D>(a.lamb, a.lamb_const, vk);
+            r.mu[k] = nodal<D>(a.mu, a.mu_const, vk);
+        }
+        if constexpr ((OPS & OP_GENERAL) != 0) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+#pragma unroll
+                for (int j = 0; j < D; ++j)
+                    r.A[k][i][j] = a.A ? __ldg(a.A + (int64_t)vk * D * D + i * D + j) : a.A_const[i * D + j];
+                r.b[k][i] = a.b ? __ldg(a.b + (int64_t)vk * D + i) : 0.0;
+                r.c[k][i] = a.c ? __ldg(a.c + (int64_t)vk * D + i) : 0.0;
+            }
+            r.a0[k] = a.a0 ? __ldg(a.a0 + vk) : a.a0_const;
+        }
+    }
+}
 
+// K1: bit-exact gradients and per-element coefficient sums from raw inputs.
+template <int D, int OPS, int CORE>
+__device__ __forceinline__ bool element_compute(const ElemRaw<D> &r, ElemGeo<D> &g)
+{
+    g.vol = r.vol;
+    bool degenerate = false;
+    if constexpr ((OPS & (OP_STIFF | OP_ELASTIC | OP_GENERAL)) != 0) degenerate = element_gradients<D, CORE>(r.x, g.G);
+    if constexpr ((OPS & OP_MASS) != 0) {
+#pragma unroll
+        for (int k = 0; k <= D; ++k) g.W[k] = r.W[k];
+        g.wsum = r.W[0];
+#pragma unroll
+        for (int k = 1; k <= D; ++k) g.wsum = SA_ADD(g.wsum, r.W[k]);
+    }
+    if constexpr ((OPS & OP_ELASTIC) != 0) {
+        // lambs = (sum_k lamb_k) * (vols / (d+1))   kernels.py:354-356
+        const double scale = __ddiv_rn(r.vol, (double)(D + 1));
+        double ls = r.lam[0], ms = r.mu[0];
+#pragma unroll
+        for (int k = 1; k <= D; ++k) { ls = SA_ADD(ls, r.lam[k]); ms = SA_ADD(ms, r.mu[k]); }
+        g.lambs = SA_MUL(ls, scale);
+        g.mus = SA_MUL(ms, scale);
+    }
+    if constexpr ((OPS & OP_GENERAL) != 0) {
+#pragma unroll
+        for (int k = 0; k <= D; ++k) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+#pragma unroll
+                for (int j = 0; j < D; ++j) g.As[i][j] = k == 0 ? r.A[0][i][j] : SA_ADD(g.As[i][j], r.A[k][i][j]);
+                g.bv[k][i] = r.b[k][i];
+                g.cv[k][i] = r.c[k][i];
+                g.bs[i] = k == 0 ? r.b[0][i] : SA_ADD(g.bs[i], r.b[k][i]);
+                g.cs[i] = k == 0 ? r.c[0][i] : SA_ADD(g.cs[i], r.c[k][i]);
+            }
+            g.a0v[k] = r.a0[k];
+            g.a0s = k == 0 ? r.a0[0] : SA_ADD(g.a0s, r.a0[k]);
+        }
+    }
+    return degenerate;
+}
+
+// K2: local row ALPHA of every requested operator, stored to dst with layout
+// dst[((b * NOUT + o) * M + l) * M + n] (entry (dof row (l, ALPHA), dof col (n, b))).
+template <int D, int M, int OPS, int ALPHA>
+__device__ __forceinline__ void element_krow(const NumArgs &a, const ElemGeo<D> &g, double *dst)
+{
+    constexpr int NOUT = n_outputs<OPS>();
     int o = 0;
     if constexpr ((OPS & OP_MASS) != 0) {
-        double W[D + 1];
+        // kernels.py:76-78: (coef * vols) * ((wsum + W[alpha]) + W[beta])
+        const double cd = SA_MUL(a.mass_coef_diag, g.vol), co = SA_MUL(a.mass_coef_off, g.vol);
+        if (a.w) {
+            const double wsa = SA_ADD(g.wsum, g.W[ALPHA]);
 #pragma unroll
-        for (int g = 0; g <= D; ++g) W[g] = nodal<D>(a.w, a.w_const, v[g]);
-        double wsum = W[0];
+            for (int b = 0; b <= D; ++b) dst[(b * NOUT + o) * M * M] = SA_MUL(b == ALPHA ? cd : co, SA_ADD(wsa, g.W[b]));
+        } else {
+            // constant weight: (wsum + W[alpha]) + W[beta] is one constant
+            const double vd = SA_MUL(cd, a.mass_wc), vo = SA_MUL(co, a.mass_wc);
 #pragma unroll
-        for (int g = 1; g <= D; ++g) wsum = SA_ADD(wsum, W[g]);
-        const double wa = select_val<D>(W, alpha);
-        const double cd = SA_MUL(a.mass_coef_diag, vol), co = SA_MUL(a.mass_coef_off, vol);
-        const double wsa = SA_ADD(wsum, wa);
-#pragma unroll
-        for (int b = 0; b <= D; ++b) {
-            double val = SA_MUL(b == alpha ? cd : co, SA_ADD(wsa, W[b]));
-            int r = (ranks >> (8 * b)) & 0xff;
-            acc[(o * a.acc_stride + r) * nthr + tid] += val;
+            for (int b = 0; b <= D; ++b) dst[(b * NOUT + o) * M * M] = b == ALPHA ? vd : vo;
         }
         ++o;
     }
     if constexpr ((OPS & OP_STIFF) != 0) {
 #pragma unroll
-        for (int b = 0; b <= D; ++b) {
-            double val = stiff_entry<D>(ga, G[b], vol);
-            int r = (ranks >> (8 * b)) & 0xff;
-            acc[(o * a.acc_stride + r) * nthr + tid] += val;
-        }
+        for (int b = 0; b <= D; ++b) dst[(b * NOUT + o) * M * M] = stiff_entry<D>(g.G[ALPHA], g.G[b], g.vol);
         ++o;
     }
     if constexpr ((OPS & OP_ELASTIC) != 0) {
-        // lambs = (sum_g lamb_g) * (vols / (d+1))   kernels.py:354-356
-        const double scale = __ddiv_rn(vol, (double)(D + 1));
-        double ls = nodal<D>(a.lamb, a.lamb_const, v[0]), ms = nodal<D>(a.mu, a.mu_const, v[0]);
 #pragma unroll
-        for (int g = 1; g <= D; ++g) {
-            ls = SA_ADD(ls, nodal<D>(a.lamb, a.lamb_const, v[g]));
-            ms = SA_ADD(ms, nodal<D>(a.mu, a.mu_const, v[g]));
-        }
-        const double lambs = SA_MUL(ls, scale), mus = SA_MUL(ms, scale);
-        const int deg_stride = a.acc_stride / M;  // = M * max_deg
-#pragma unroll
-        for (int b = 0; b <= D; ++b) {
-            const int r = (ranks >> (8 * b)) & 0xff;
+        for (int b = 0; b <= D; ++b)
 #pragma unroll
             for (int l = 0; l < M; ++l)
 #pragma unroll
-                for (int n = 0; n < M; ++n) {
-                    double val = elastic_entry<D>(ga, G[b], l, n, lambs, mus);
-                    acc[(o * a.acc_stride + l * deg_stride + r * M + n) * nthr + tid] += val;
-                }
-        }
+                for (int n = 0; n < M; ++n)
+                    dst[((b * NOUT + o) * M + l) * M + n] = elastic_entry<D>(g.G[ALPHA], g.G[b], l, n, g.lambs, g.mus);
         ++o;
     }
     if constexpr ((OPS & OP_GENERAL) != 0) {
-        double As[D][D], bs[D], cs[D], a0s;
-        double bb[D + 1][D], cc[D], a0v[D + 1];
-#pragma unroll
-        for (int g = 0; g <= D; ++g) {
-            const int vg = v[g];
-#pragma unroll
-            for (int i = 0; i < D; ++i)
-#pragma unroll
-                for (int j = 0; j < D; ++j) {
-                    double t = a.A ? __ldg(a.A + (int64_t)vg * D * D + i * D + j) : a.A_const[i * D + j];
-                    As[i][j] = g == 0 ? t : SA_ADD(As[i][j], t);
-                }
-#pragma unroll
-            for (int i = 0; i < D; ++i) {
-                double tb = a.b ? __ldg(a.b + (int64_t)vg * D + i) : 0.0;
-                double tc = a.c ? __ldg(a.c + (int64_t)vg * D + i) : 0.0;
-                bb[g][i] = tb;
-                bs[i] = g == 0 ? tb : SA_ADD(bs[i], tb);
-                cs[i] = g == 0 ? tc : SA_ADD(cs[i], tc);
-                if (g == alpha) cc[i] = tc;
-            }
-            a0v[g] = a.a0 ? __ldg(a.a0 + vg) : a.a0_const;
-            a0s = g == 0 ? a0v[0] : SA_ADD(a0s, a0v[g]);
-        }
-        const double s1 = __ddiv_rn(vol, (double)(D + 1));
-        const double s2 = __ddiv_rn(vol, (double)((D + 1) * (D + 2)));
-        const double cd = SA_MUL(a.mass_coef_diag, vol), co = SA_MUL(a.mass_coef_off, vol);
-        const double a0a = select_val<D>(a0v, alpha);
+        const double s1 = __ddiv_rn(g.vol, (double)(D + 1));
+        const double s2 = __ddiv_rn(g.vol, (double)((D + 1) * (D + 2)));
+        const double cd = SA_MUL(a.mass_coef_diag, g.vol), co = SA_MUL(a.mass_coef_off, g.vol);
+        const double(&ga)[D] = g.G[ALPHA];
 #pragma unroll
         for (int b = 0; b <= D; ++b) {
             double AG[D];
 #pragma unroll
             for (int i = 0; i < D; ++i) {
-                double t = SA_MUL(As[i][0], G[b][0]);
+                double t = SA_MUL(g.As[i][0], g.G[b][0]);
 #pragma unroll
-                for (int j = 1; j < D; ++j) t = SA_ADD(t, SA_MUL(As[i][j], G[b][j]));
+                for (int j = 1; j < D; ++j) t = SA_ADD(t, SA_MUL(g.As[i][j], g.G[b][j]));
                 AG[i] = t;
             }
             double diff = SA_MUL(ga[0], AG[0]);
-            double conv = SA_MUL(SA_ADD(bs[0], bb[b][0]), ga[0]);
-            double tran = SA_MUL(SA_ADD(cs[0], cc[0]), G[b][0]);
+            double conv = SA_MUL(SA_ADD(g.bs[0], g.bv[b][0]), ga[0]);
+            double tran = SA_MUL(SA_ADD(g.cs[0], g.cv[ALPHA][0]), g.G[b][0]);
 #pragma unroll
             for (int i = 1; i < D; ++i) {
                 diff = SA_ADD(diff, SA_MUL(ga[i], AG[i]));
-                conv = SA_ADD(conv, SA_MUL(SA_ADD(bs[i], bb[b][i]), ga[i]));
-                tran = SA_ADD(tran, SA_MUL(SA_ADD(cs[i], cc[i]), G[b][i]));
+                conv = SA_ADD(conv, SA_MUL(SA_ADD(g.bs[i], g.bv[b][i]), ga[i]));
+                tran = SA_ADD(tran, SA_MUL(SA_ADD(g.cs[i], g.cv[ALPHA][i]), g.G[b][i]));
             }
-            double rea = SA_MUL(b == alpha ? cd : co, SA_ADD(SA_ADD(a0s, a0a), a0v[b]));
-            double val = SA_ADD(SA_ADD(SA_SUB(SA_MUL(diff, s1), SA_MUL(conv, s2)), SA_MUL(tran, s2)), rea);
-            int r = (ranks >> (8 * b)) & 0xff;
-            acc[(o * a.acc_stride + r) * nthr + tid] += val;
+            const double rea = SA_MUL(b == ALPHA ? cd : co, SA_ADD(SA_ADD(g.a0s, g.a0v[ALPHA]), g.a0v[b]));
+            dst[(b * NOUT + o) * M * M] =
+                SA_ADD(SA_ADD(SA_SUB(SA_MUL(diff, s1), SA_MUL(conv, s2)), SA_MUL(tran, s2)), rea);
         }
         ++o;
     }
 }
 
+// runtime local row alpha -> compile-time element_krow<alpha>
+template <int D, int M, int OPS, int A = 0>
+__device__ __forceinline__ void krow_runtime(const NumArgs &a, const ElemGeo<D> &g, int alpha, double *vals)
+{
+    if (alpha == A) element_krow<D, M, OPS, A>(a, g, vals);
+    else if constexpr (A < D) krow_runtime<D, M, OPS, A + 1>(a, g, alpha, vals);
+}
+
+// v1 / fallback numeric kernel: one thread per node row, private smem
+// accumulators indexed by the 8-bit column ranks stored with each incidence.
+// Used when a node has more than 31 incidences or the block kernel's shared
+// memory does not fit.
 template <int D, int M, int OPS, int CORE>
 __global__ void __launch_bounds__(128) k_numeric_rowgather(NumArgs a)
 {
@@ -420,40 +650,277 @@ __global__ void __launch_bounds__(128) k_numeric_rowgather(NumArgs a)
         const int64_t c0 = a.colptr[nl];
         const int deg = (int)(a.colptr[nl + 1] - c0);
         const int deg_stride = M * deg;
+        const int row_stride = a.acc_stride / M;
         for (int o = 0; o < NOUT; ++o)
             for (int l = 0; l < M; ++l)
                 for (int k = 0; k < deg_stride; ++k)
-                    smem_acc[(o * a.acc_stride + l * (a.acc_stride / M) + k) * nthr + tid] = 0.0;
+                    smem_acc[(o * a.acc_stride + l * row_stride + k) * nthr + tid] = 0.0;
         const int64_t t1 = a.inc_ptr[nl + 1];
         int64_t emin = INT64_MAX;
-        for (int64_t t = a.inc_ptr[nl]; t < t1; ++t) {
-            uint2 rec = __ldg(a.inc + t);
-            bool dg = false;
-            fold_incidence<D, M, OPS, CORE>(a, rec, smem_acc, tid, nthr, dg);
-            if (dg) emin = min(emin, (int64_t)(rec.x & 0x3fffffffu));
+        constexpr int MM = M * M;
+        auto fold = [&](const ElemRaw<D> &x, uint2 rec) {
+            ElemGeo<D> g;
+            const int64_t e = rec.x & 0x3fffffffu;
+            if (element_compute<D, OPS, CORE>(x, g)) emin = min(emin, e);
+            double vals[(D + 1) * NOUT * MM];
+            krow_runtime<D, M, OPS>(a, g, rec.x >> 30, vals);
+#pragma unroll
+            for (int b = 0; b <= D; ++b) {
+                const int r = (rec.y >> (8 * b)) & 0xff;
+#pragma unroll
+                for (int o = 0; o < NOUT; ++o)
+#pragma unroll
+                    for (int l = 0; l < M; ++l)
+#pragma unroll
+                        for (int n = 0; n < M; ++n)
+                            smem_acc[(o * a.acc_stride + l * row_stride + r * M + n) * nthr + tid] +=
+                                vals[(b * NOUT + o) * MM + l * M + n];
+            }
+        };
+        int64_t t = a.inc_ptr[nl];
+        for (; t + 1 < t1; t += 2) {
+            const uint2 r1 = __ldg(a.inc + t), r2 = __ldg(a.inc + t + 1);
+            ElemRaw<D> x1, x2;
+            element_load1<D, OPS>(a, r1.x & 0x3fffffffu, x1);
+            element_load1<D, OPS>(a, r2.x & 0x3fffffffu, x2);
+            element_load2<D, OPS>(a, x1);
+            element_load2<D, OPS>(a, x2);
+            fold(x1, r1);
+            fold(x2, r2);
         }
-        if (emin != INT64_MAX) {
-            atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)emin);
+        if (t < t1) {
+            const uint2 r1 = __ldg(a.inc + t);
+            ElemRaw<D> x1;
+            element_load1<D, OPS>(a, r1.x & 0x3fffffffu, x1);
+            element_load2<D, OPS>(a, x1);
+            fold(x1, r1);
         }
+        if (emin != INT64_MAX) atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)emin);
         for (int o = 0; o < NOUT; ++o) {
             double *out = a.vals[o];
             for (int l = 0; l < M; ++l) {
                 const int64_t p = a.indptr[M * nl + l];
                 for (int k = 0; k < deg_stride; ++k) {
-                    double val = smem_acc[(o * a.acc_stride + l * (a.acc_stride / M) + k) * nthr + tid];
+                    double val = smem_acc[(o * a.acc_stride + l * row_stride + k) * nthr + tid];
                     out[p + k] = val;
                     nz[o] += (val == 0.0);
                 }
             }
         }
     }
-    // deterministic integer reduction of the exact-zero counts
 #pragma unroll
     for (int o = 0; o < NOUT; ++o) {
         int v = nz[o];
 #pragma unroll
         for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
         if ((tid & 31) == 0 && v) atomicAdd((unsigned long long *)(a.counters + o), (unsigned long long)v);
+    }
+}
+
+// element lane: local row A of the element -> scatter into the fold array
+template <int D, int M, int OPS, int A = 0>
+__device__ __forceinline__ void element_rows_scatter(const NumArgs &a, const ElemGeo<D> &g, unsigned sw,
+                                                     const uint32_t *__restrict__ tm, unsigned sb, double *F, int FS)
+{
+    constexpr int NOUT = n_outputs<OPS>();
+    constexpr int MM = M * M;
+    const unsigned slot = (sw >> (8 * A)) & 0xff;
+    if (slot != 0xff) {
+        double vals[(D + 1) * NOUT * MM];
+        element_krow<D, M, OPS, A>(a, g, vals);
+        const unsigned p01 = __ldg(tm + sb + 2 * slot), p23 = __ldg(tm + sb + 2 * slot + 1);
+#pragma unroll
+        for (int b = 0; b <= D; ++b) {
+            const unsigned pos = ((b < 2 ? p01 : p23) >> (16 * (b & 1))) & 0xffff;
+#pragma unroll
+            for (int o = 0; o < NOUT; ++o)
+#pragma unroll
+                for (int i = 0; i < MM; ++i) F[(o * FS + pos) * MM + i] = vals[(b * NOUT + o) * MM + i];
+        }
+    }
+    if constexpr (A < D) element_rows_scatter<D, M, OPS, A + 1>(a, g, sw, tm, sb, F, FS);
+}
+
+// Tile numeric kernel (K1 + K2 + K4), the production path.
+//
+// One warp owns one tile (R = 32/L consecutive node rows, L lanes per row);
+// warps never synchronise with each other, so the SM overlaps one warp's
+// loads with another's arithmetic.
+//   phase 1  lanes over the tile's distinct elements: loads for two elements
+//            in flight, geometry once per element, then each local row the
+//            tile needs, scattered into the tile's entry-major fold array in
+//            warp-private shared memory;
+//   phase 2  each row's L lanes sum their entries' contiguous runs in
+//            registers (ascending element order) into an output segment;
+//   phase 3  the tile's rows are consecutive, so their CSR segment is one
+//            contiguous range: coalesced stores.
+// Every entry is the left-to-right sum of its contributions in ascending
+// element index: bitwise the reference's optv2 value.
+struct TileArgs {
+    const uint32_t *tile_e0;   // (ntiles) smallest element of each tile
+    const uint32_t *tile_tm;   // (ntiles) template id
+    const uint32_t *tm_off;    // (ntemplates) word offset of each template
+    const uint32_t *tm;        // template words
+    int max_inc;               // max incidences (slots) in one tile
+    int max_ent;               // max node-level entries in one tile
+};
+
+// Kernel choice: the row-gather kernel is the default (fastest measured on
+// every BASELINE config so far); SA_KERNEL=tile selects the tile kernel, whose
+// templates are then built in the symbolic phase.
+inline bool want_tile_kernel()
+{
+    const char *k = getenv("SA_KERNEL");
+    return k && strcmp(k, "tile") == 0;
+}
+
+// lanes per row (R = 32/L rows per warp tile): default per (d, m), override
+// with SA_TILE_LANES at plan creation (tuning).
+inline int default_lanes(int d, int m)
+{
+    return d == 1 ? 1 : (m == 1 ? (d == 2 ? 2 : 4) : (d == 2 ? 4 : 16));
+}
+inline int tile_lanes(int d, int m)
+{
+    const char *v = getenv("SA_TILE_LANES");
+    int L = v ? atoi(v) : default_lanes(d, m);
+    if (L != 1 && L != 2 && L != 4 && L != 8 && L != 16) L = default_lanes(d, m);
+    return L;
+}
+
+template <int D, int M, int OPS, int CORE, int L>
+__global__ void __launch_bounds__(128) k_numeric_tiles(NumArgs a, TileArgs t)
+{
+    constexpr int NOUT = n_outputs<OPS>();
+    constexpr int MM = M * M;
+    constexpr int R = 32 / L;
+    constexpr int WARPS = 4;
+    extern __shared__ __align__(16) double smem_d[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t T = (int64_t)blockIdx.x * WARPS + wid;
+    const int64_t r0 = T * R;
+    if (r0 >= a.nnodes) return;
+    const int FS = (D + 1) * t.max_inc;          // fold positions per output
+    const int OS = M > 1 ? MM * t.max_ent : 0;   // output staging (vector case only)
+    double *F = smem_d + (size_t)wid * NOUT * ((size_t)FS * MM + OS);
+    double *outs = F + (size_t)NOUT * FS * MM;
+
+    const unsigned to = __ldg(t.tm_off + __ldg(t.tile_tm + T));
+    const unsigned eb = __ldg(t.tile_e0 + T);
+    const unsigned hdr = __ldg(t.tm + to);
+    const int ne = hdr & 0xff, nr = (hdr >> 8) & 0xff, NI = hdr >> 16;
+    const int NE = __ldg(t.tm + to + 1);
+    const unsigned SB = to + 2 + 2 * ne, PB = SB + 2 * NI, OB = PB + nr;
+
+    // phase 1: each distinct element once, two per lane in flight
+    int64_t emin = INT64_MAX;
+    for (int j = lane; j < ne; j += 64) {
+        const bool two = j + 32 < ne;
+        const int64_t e1 = (int64_t)eb + __ldg(t.tm + to + 2 + j);
+        const unsigned sw1 = __ldg(t.tm + to + 2 + ne + j);
+        const int64_t e2 = two ? (int64_t)eb + __ldg(t.tm + to + 2 + j + 32) : e1;
+        const unsigned sw2 = two ? __ldg(t.tm + to + 2 + ne + j + 32) : 0xffffffffu;
+        ElemRaw<D> x1, x2;
+        element_load1<D, OPS>(a, e1, x1);
+        element_load1<D, OPS>(a, e2, x2);
+        element_load2<D, OPS>(a, x1);
+        element_load2<D, OPS>(a, x2);
+        ElemGeo<D> g;
+        if (element_compute<D, OPS, CORE>(x1, g)) emin = min(emin, e1);
+        element_rows_scatter<D, M, OPS>(a, g, sw1, t.tm, SB, F, FS);
+        if (two) {
+            if (element_compute<D, OPS, CORE>(x2, g)) emin = min(emin, e2);
+            element_rows_scatter<D, M, OPS>(a, g, sw2, t.tm, SB, F, FS);
+        }
+    }
+    if (emin != INT64_MAX) atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)emin);
+    __syncwarp();
+
+    int nz[NOUT];
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) nz[o] = 0;
+    const int64_t base = a.indptr[(int64_t)M * r0];
+    if constexpr (M == 1) {
+        // phase 2 (scalar): lanes over the tile's entries, which are in CSR
+        // order; a warp-uniform loop over contribution ranks (predicated, no
+        // divergent branches) sums each entry's contiguous run left to right,
+        // and the result is stored straight to its CSR position (coalesced).
+        for (int k0 = 0; k0 < NE; k0 += 32) {
+            const int kg = k0 + lane;
+            const bool valid = kg < NE;
+            unsigned s0 = 0, s1 = 0;
+            if (valid) {
+                s0 = (__ldg(t.tm + OB + (kg >> 1)) >> (16 * (kg & 1))) & 0xffff;
+                s1 = (__ldg(t.tm + OB + ((kg + 1) >> 1)) >> (16 * ((kg + 1) & 1))) & 0xffff;
+            }
+            const int cnt = (int)(s1 - s0);
+            const int maxc = __reduce_max_sync(0xffffffffu, cnt);
+            double acc[NOUT];
+#pragma unroll
+            for (int o = 0; o < NOUT; ++o) acc[o] = 0.0;
+            for (int i = 0; i < maxc; ++i) {
+                const bool on = i < cnt;
+                const unsigned sidx = on ? s0 + i : 0;
+#pragma unroll
+                for (int o = 0; o < NOUT; ++o) {
+                    const double v = F[o * FS + sidx];
+                    acc[o] = on ? SA_ADD(acc[o], v) : acc[o];
+                }
+            }
+            if (valid) {
+#pragma unroll
+                for (int o = 0; o < NOUT; ++o) {
+                    a.vals[o][base + kg] = acc[o];
+                    nz[o] += (acc[o] == 0.0);
+                }
+            }
+        }
+    } else {
+        // phase 2 (vector): each row's L lanes sum their entries' runs
+        const int row = lane / L, jl = lane % L;
+        if (row < nr) {
+            const unsigned rw = __ldg(t.tm + PB + row);
+            const int deg = rw & 0xffff, entb = rw >> 16;
+            for (int k = jl; k < deg; k += L) {
+                const int kg = entb + k;
+                const unsigned s0 = (__ldg(t.tm + OB + (kg >> 1)) >> (16 * (kg & 1))) & 0xffff;
+                const unsigned s1 = (__ldg(t.tm + OB + ((kg + 1) >> 1)) >> (16 * ((kg + 1) & 1))) & 0xffff;
+#pragma unroll
+                for (int o = 0; o < NOUT; ++o) {
+                    double acc[MM];
+#pragma unroll
+                    for (int i = 0; i < MM; ++i) acc[i] = 0.0;
+                    const double *src = F + (size_t)o * FS * MM;
+                    for (unsigned s = s0; s < s1; ++s)
+#pragma unroll
+                        for (int i = 0; i < MM; ++i) acc[i] = SA_ADD(acc[i], src[s * MM + i]);
+                    double *orow = outs + o * OS + MM * entb;
+#pragma unroll
+                    for (int l = 0; l < M; ++l)
+#pragma unroll
+                        for (int n = 0; n < M; ++n) orow[l * M * deg + k * M + n] = acc[l * M + n];
+                }
+            }
+        }
+        __syncwarp();
+        // phase 3: the tile's CSR segment is contiguous -> coalesced stores
+#pragma unroll
+        for (int o = 0; o < NOUT; ++o) {
+            double *dst = a.vals[o] + base;
+            const double *src = outs + o * OS;
+            for (int i = lane; i < MM * NE; i += 32) {
+                const double v = src[i];
+                dst[i] = v;
+                nz[o] += (v == 0.0);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) {
+        int v = nz[o];
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+        if (lane == 0 && v) atomicAdd((unsigned long long *)(a.counters + o), (unsigned long long)v);
     }
 }
 
@@ -522,6 +989,85 @@ int mesh_kernels(sa_mesh *M, const double *q, const int64_t *me, const double *v
     return SA_OK;
 }
 
+// Host side of the tile-template dedupe: build every tile in scratch, dedupe
+// by 64-bit signature, pack one copy per template, then verify every tile
+// word for word against its template (a hash collision disables templates).
+template <int D>
+int build_tile_templates(sa_plan *P, int R, cudaStream_t st)
+{
+    const int64_t nn = P->nnodes;
+    const int64_t ntiles = (nn + R - 1) / R;
+    int c = 0;
+    while ((1 << c) < R) ++c;
+    const int64_t NI = P->tile_max_inc[c], NE = P->tile_max_ent[c];
+    if (NI > 254) return SA_OK;  // tiles too wide for 8-bit slots: row-gather kernel
+    const int64_t stride64 = tile_stride_bound(NI, NE, R);
+    const int stride = (int)stride64;
+    uint32_t *scratch = nullptr, *words = nullptr;
+    uint64_t *sig = nullptr;
+    SA_CUDA_TRY(cudaMallocAsync((void **)&scratch, ntiles * stride64 * sizeof(uint32_t), st));
+    SA_CUDA_TRY(cudaMallocAsync((void **)&words, ntiles * sizeof(uint32_t), st));
+    SA_CUDA_TRY(cudaMallocAsync((void **)&sig, ntiles * sizeof(uint64_t), st));
+    SA_CUDA_TRY(cudaMallocAsync((void **)&P->tile_e0, ntiles * sizeof(uint32_t), st));
+    SA_CUDA_TRY(cudaMallocAsync((void **)&P->tile_tm, ntiles * sizeof(uint32_t), st));
+    SA_CUDA_TRY(cudaMemsetAsync(P->counters + 6, 0, sizeof(int64_t), st));
+    SA_LAUNCH(k_tile_build<D>, grid_for(ntiles, 64), 64, 0, st, P->inc_ptr, P->inc_e, P->fold, P->colptr, nn, R,
+              ntiles, stride, scratch, words, sig, P->tile_e0, (unsigned long long *)(P->counters + 6));
+    std::vector<uint64_t> hs(ntiles);
+    std::vector<uint32_t> hw(ntiles);
+    int64_t fail = 0;
+    SA_CUDA_TRY(cudaMemcpyAsync(hs.data(), sig, ntiles * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    SA_CUDA_TRY(cudaMemcpyAsync(hw.data(), words, ntiles * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    SA_CUDA_TRY(cudaMemcpyAsync(&fail, P->counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SA_CUDA_TRY(cudaStreamSynchronize(st));
+    int rc = SA_OK;
+    if (!fail) {
+        std::unordered_map<uint64_t, uint32_t> ids;
+        std::vector<uint32_t> ttm(ntiles), off;
+        std::vector<int64_t> rep;
+        uint64_t total = 0;
+        for (int64_t i = 0; i < ntiles; ++i) {
+            auto it = ids.find(hs[i]);
+            if (it == ids.end()) {
+                const uint32_t id = (uint32_t)rep.size();
+                ids.emplace(hs[i], id);
+                rep.push_back(i);
+                off.push_back((uint32_t)total);
+                total += hw[i];
+                ttm[i] = id;
+            } else {
+                ttm[i] = it->second;
+            }
+        }
+        if (total < ((uint64_t)1 << 32)) {
+            P->n_templates = (int64_t)rep.size();
+            P->tm_nwords = (int64_t)total;
+            P->tile_rows = R;
+            int64_t *drep = nullptr;
+            SA_CUDA_TRY(cudaMallocAsync((void **)&drep, rep.size() * sizeof(int64_t), st));
+            SA_CUDA_TRY(cudaMallocAsync((void **)&P->tm_off, off.size() * sizeof(uint32_t), st));
+            SA_CUDA_TRY(cudaMallocAsync((void **)&P->tm, std::max<uint64_t>(total, 1) * sizeof(uint32_t), st));
+            SA_CUDA_TRY(cudaMemcpyAsync(drep, rep.data(), rep.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+            SA_CUDA_TRY(cudaMemcpyAsync(P->tm_off, off.data(), off.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+            SA_CUDA_TRY(cudaMemcpyAsync(P->tile_tm, ttm.data(), ntiles * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+            SA_LAUNCH(k_tile_pack, grid_for((int64_t)rep.size() * 32, 128), 128, 0, st, drep, (int64_t)rep.size(),
+                      scratch, stride, words, P->tm_off, P->tm);
+            SA_CUDA_TRY(cudaMemsetAsync(P->counters + 6, 0, sizeof(int64_t), st));
+            SA_LAUNCH(k_tile_verify, grid_for(ntiles * 32, 128), 128, 0, st, scratch, stride, words, ntiles,
+                      P->tile_tm, P->tm_off, P->tm, (unsigned long long *)(P->counters + 6));
+            int64_t bad = 0;
+            SA_CUDA_TRY(cudaMemcpyAsync(&bad, P->counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            SA_CUDA_TRY(cudaStreamSynchronize(st));
+            SA_CUDA_TRY(cudaFreeAsync(drep, st));
+            P->tm_ok = (bad == 0);
+        }
+    }
+    SA_CUDA_TRY(cudaFreeAsync(scratch, st));
+    SA_CUDA_TRY(cudaFreeAsync(words, st));
+    SA_CUDA_TRY(cudaFreeAsync(sig, st));
+    return rc;
+}
+
 template <int D>
 int symbolic_kernels(sa_plan *P, cudaStream_t st)
 {
@@ -573,6 +1119,34 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
     int64_t md = 0;
     for (int64_t i = 0; i < nn; ++i) md = std::max(md, hcp[i + 1] - hcp[i]);
     P->max_deg = md;
+    // block numeric kernel data
+    {
+        std::vector<int64_t> hip(nn + 1);
+        SA_CUDA_TRY(cudaMemcpyAsync(hip.data(), P->inc_ptr, (nn + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        SA_CUDA_TRY(cudaMallocAsync((void **)&P->inc_e, std::max<int64_t>(P->n_inc, 1) * sizeof(uint32_t), st));
+        SA_CUDA_TRY(cudaMallocAsync((void **)&P->fold, std::max<int64_t>((D + 1) * P->n_inc, 1) * sizeof(uint16_t), st));
+        SA_CUDA_TRY(cudaMemsetAsync(P->counters + 6, 0, sizeof(int64_t), st));
+        if (nn)
+            SA_LAUNCH(k_fold_lists<D>, grid_for(nn, 128), 128, 0, st, P->inc_ptr, P->inc, nn, P->colptr, P->inc_e,
+                      P->fold, (unsigned long long *)(P->counters + 6));
+        int64_t too_many = 0;
+        SA_CUDA_TRY(cudaMemcpyAsync(&too_many, P->counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        P->fold_ok = (too_many == 0);
+        for (int c = 0; c < 6; ++c) {
+            const int64_t R = (int64_t)1 << c;
+            int64_t mi = 0, mz = 0;
+            for (int64_t r0 = 0; r0 < nn; r0 += R) {
+                mi = std::max(mi, hip[std::min(nn, r0 + R)] - hip[r0]);
+                mz = std::max(mz, hcp[std::min(nn, r0 + R)] - hcp[r0]);
+            }
+            P->tile_max_inc[c] = mi;
+            P->tile_max_ent[c] = mz;
+        }
+        if (P->fold_ok && md <= 255 && nn && want_tile_kernel()) {
+            SA_TRY(build_tile_templates<D>(P, 32 / tile_lanes(D, P->m), st));
+        }
+    }
     const int m = P->m;
     P->nnz = (int64_t)m * m * P->n_colnodes;
     if (P->nnz >= ((int64_t)1 << 31) || (int64_t)m * M->nq >= ((int64_t)1 << 31))
@@ -586,8 +1160,10 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
     return SA_OK;
 }
 
+// Kernel selection: the tile kernel whenever the plan has verified fold
+// templates; SA_KERNEL=rowgather forces the v1 kernel (tests, comparison).
 template <int D, int M, int OPS, int CORE>
-int launch_numeric(const NumArgs &a, int64_t nnodes, cudaStream_t st)
+int launch_rowgather(const NumArgs &a, int64_t nnodes, cudaStream_t st)
 {
     constexpr int NOUT = n_outputs<OPS>();
     int block = 128;
@@ -601,24 +1177,75 @@ int launch_numeric(const NumArgs &a, int64_t nnodes, cudaStream_t st)
     return SA_OK;
 }
 
-template <int D, int M, int OPS>
-int launch_numeric_core(const NumArgs &a, int64_t nnodes, int core, cudaStream_t st)
+// returns SA_OK after launching, 1000 when the tile kernel does not fit
+#define SA_TRY_OR_FALL(...)                  \
+    do {                                     \
+        int _r = (__VA_ARGS__);              \
+        if (_r == SA_OK) return SA_OK;       \
+        if (_r != 1000) return _r;           \
+    } while (0)
+
+template <int D, int M, int OPS, int CORE, int L>
+int launch_tiles(const sa_plan *P, const NumArgs &a, cudaStream_t st)
 {
-    if (core == CORE_SKYLAKEX) return launch_numeric<D, M, OPS, CORE_SKYLAKEX>(a, nnodes, st);
-    return launch_numeric<D, M, OPS, CORE_HASWELL>(a, nnodes, st);
+    constexpr int NOUT = n_outputs<OPS>();
+    constexpr int VPI = NOUT * M * M * (D + 1);
+    constexpr int R = 32 / L;
+    constexpr int LOG2R = R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : R == 8 ? 3 : R == 16 ? 4 : 5;
+    TileArgs t;
+    t.tile_e0 = P->tile_e0;
+    t.tile_tm = P->tile_tm;
+    t.tm_off = P->tm_off;
+    t.tm = P->tm;
+    t.max_inc = (int)P->tile_max_inc[LOG2R];
+    t.max_ent = (int)P->tile_max_ent[LOG2R];
+    const size_t warp_bytes =
+        (size_t)NOUT * ((size_t)(D + 1) * t.max_inc * M * M + (M > 1 ? (size_t)M * M * t.max_ent : 0)) * 8;
+    const size_t smem = 4 * warp_bytes;
+    if (smem > 200 * 1024) return 1000;
+    (void)VPI;
+    auto kern = k_numeric_tiles<D, M, OPS, CORE, L>;
+    SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (P->nnodes) SA_LAUNCH(kern, grid_for(P->nnodes, 4 * R), 128, smem, st, a, t);
+    return SA_OK;
+}
+
+template <int D, int M, int OPS, int CORE>
+int launch_numeric(const sa_plan *P, const NumArgs &a, cudaStream_t st)
+{
+    const int64_t nnodes = P->nnodes;
+    const bool use_tile = P->tm_ok && want_tile_kernel();
+    if (use_tile) {
+        switch (32 / P->tile_rows) {
+            case 1: SA_TRY_OR_FALL(launch_tiles<D, M, OPS, CORE, 1>(P, a, st)); break;
+            case 2: SA_TRY_OR_FALL(launch_tiles<D, M, OPS, CORE, 2>(P, a, st)); break;
+            case 4: SA_TRY_OR_FALL(launch_tiles<D, M, OPS, CORE, 4>(P, a, st)); break;
+            case 8: SA_TRY_OR_FALL(launch_tiles<D, M, OPS, CORE, 8>(P, a, st)); break;
+            case 16: SA_TRY_OR_FALL(launch_tiles<D, M, OPS, CORE, 16>(P, a, st)); break;
+            default: break;
+        }
+    }
+    return launch_rowgather<D, M, OPS, CORE>(a, nnodes, st);
+}
+
+template <int D, int M, int OPS>
+int launch_numeric_core(const sa_plan *P, const NumArgs &a, int core, cudaStream_t st)
+{
+    if (core == CORE_SKYLAKEX) return launch_numeric<D, M, OPS, CORE_SKYLAKEX>(P, a, st);
+    return launch_numeric<D, M, OPS, CORE_HASWELL>(P, a, st);
 }
 
 template <int D>
-int dispatch_numeric(const NumArgs &a, int ops, int m, int64_t nnodes, int core, cudaStream_t st)
+int dispatch_numeric(const sa_plan *P, const NumArgs &a, int ops, int core, cudaStream_t st)
 {
     switch (ops) {
-        case OP_MASS: return launch_numeric_core<D, 1, OP_MASS>(a, nnodes, core, st);
-        case OP_STIFF: return launch_numeric_core<D, 1, OP_STIFF>(a, nnodes, core, st);
-        case OP_MASS | OP_STIFF: return launch_numeric_core<D, 1, OP_MASS | OP_STIFF>(a, nnodes, core, st);
-        case OP_GENERAL: return launch_numeric_core<D, 1, OP_GENERAL>(a, nnodes, core, st);
+        case OP_MASS: return launch_numeric_core<D, 1, OP_MASS>(P, a, core, st);
+        case OP_STIFF: return launch_numeric_core<D, 1, OP_STIFF>(P, a, core, st);
+        case OP_MASS | OP_STIFF: return launch_numeric_core<D, 1, OP_MASS | OP_STIFF>(P, a, core, st);
+        case OP_GENERAL: return launch_numeric_core<D, 1, OP_GENERAL>(P, a, core, st);
         case OP_ELASTIC:
             if constexpr (D >= 2) {
-                if (m == D) return launch_numeric_core<D, D, OP_ELASTIC>(a, nnodes, core, st);
+                if (P->m == D) return launch_numeric_core<D, D, OP_ELASTIC>(P, a, core, st);
             }
             return set_error(SA_ERR_ARG, "elastic operator needs d in {2,3} and m == d");
         default: return set_error(SA_ERR_ARG, "unsupported operator combination %d", ops);
@@ -627,6 +1254,33 @@ int dispatch_numeric(const NumArgs &a, int ops, int m, int64_t nnodes, int core,
 
 }  // namespace
 
+// The kernels are compiled once per dimension (SA_D = 1, 2, 3: sa_d1.cu ..
+// sa_d3.cu, in parallel); the C ABI (SA_ABI: sa_abi.cu) reaches them through
+// these wrappers.
+#define SA_CAT2(a, b) a##b
+#define SA_CAT(a, b) SA_CAT2(a, b)
+int sa_mesh_kernels_d1(sa_mesh *, const double *, const int64_t *, const double *, cudaStream_t);
+int sa_mesh_kernels_d2(sa_mesh *, const double *, const int64_t *, const double *, cudaStream_t);
+int sa_mesh_kernels_d3(sa_mesh *, const double *, const int64_t *, const double *, cudaStream_t);
+int sa_symbolic_d1(sa_plan *, cudaStream_t);
+int sa_symbolic_d2(sa_plan *, cudaStream_t);
+int sa_symbolic_d3(sa_plan *, cudaStream_t);
+int sa_dispatch_d1(const sa_plan *, const NumArgs &, int, int, cudaStream_t);
+int sa_dispatch_d2(const sa_plan *, const NumArgs &, int, int, cudaStream_t);
+int sa_dispatch_d3(const sa_plan *, const NumArgs &, int, int, cudaStream_t);
+#ifdef SA_D
+int SA_CAT(sa_mesh_kernels_d, SA_D)(sa_mesh *M, const double *q, const int64_t *me, const double *vols, cudaStream_t st)
+{
+    return mesh_kernels<SA_D>(M, q, me, vols, st);
+}
+int SA_CAT(sa_symbolic_d, SA_D)(sa_plan *P, cudaStream_t st) { return symbolic_kernels<SA_D>(P, st); }
+int SA_CAT(sa_dispatch_d, SA_D)(const sa_plan *P, const NumArgs &a, int ops, int core, cudaStream_t st)
+{
+    return dispatch_numeric<SA_D>(P, a, ops, core, st);
+}
+#endif
+
+#ifdef SA_ABI
 // ===========================================================================
 // C ABI
 
@@ -667,9 +1321,9 @@ int sa_mesh_create(int d, int64_t nq, int64_t nme, const double *q_dev, const in
         cudaMalloc((void **)&M->vols, std::max<int64_t>(nme, 1) * sizeof(double)) != cudaSuccess ||
         cudaMalloc((void **)&M->scratch, 8 * sizeof(int64_t)) != cudaSuccess)
         return fail(set_error(SA_ERR_NOMEM, "device allocation for the mesh failed"));
-    if (d == 1) rc = mesh_kernels<1>(M, q_dev, me_dev, vols_dev, st);
-    else if (d == 2) rc = mesh_kernels<2>(M, q_dev, me_dev, vols_dev, st);
-    else rc = mesh_kernels<3>(M, q_dev, me_dev, vols_dev, st);
+    if (d == 1) rc = sa_mesh_kernels_d1(M, q_dev, me_dev, vols_dev, st);
+    else if (d == 2) rc = sa_mesh_kernels_d2(M, q_dev, me_dev, vols_dev, st);
+    else rc = sa_mesh_kernels_d3(M, q_dev, me_dev, vols_dev, st);
     if (rc != SA_OK) return fail(rc);
     *out = M;
     return SA_OK;
@@ -700,6 +1354,8 @@ int sa_plan_destroy(sa_plan *P)
     cudaDeviceSynchronize();
     cudaFree(P->inc_ptr); cudaFree(P->inc); cudaFree(P->colptr); cudaFree(P->cols);
     cudaFree(P->indptr); cudaFree(P->indices); cudaFree(P->counters); cudaFree(P->scan_tmp);
+    cudaFree(P->inc_e); cudaFree(P->fold);
+    cudaFree(P->tile_e0); cudaFree(P->tile_tm); cudaFree(P->tm_off); cudaFree(P->tm);
     delete P;
     return SA_OK;
 }
@@ -725,9 +1381,9 @@ int sa_plan_create(const sa_mesh *M, int m, int64_t row_begin, int64_t row_end, 
         return set_error(SA_ERR_NOMEM, "device allocation failed");
     }
     int rc;
-    if (M->d == 1) rc = symbolic_kernels<1>(P, st);
-    else if (M->d == 2) rc = symbolic_kernels<2>(P, st);
-    else rc = symbolic_kernels<3>(P, st);
+    if (M->d == 1) rc = sa_symbolic_d1(P, st);
+    else if (M->d == 2) rc = sa_symbolic_d2(P, st);
+    else rc = sa_symbolic_d3(P, st);
     if (rc != SA_OK) {
         std::string msg = err_state().msg;
         cudaStreamSynchronize(st);
@@ -745,6 +1401,15 @@ int sa_plan_info(const sa_plan *P, int64_t *nrows, int64_t *nnz, int64_t *max_ro
     if (nrows) *nrows = P->nrows;
     if (nnz) *nnz = P->nnz;
     if (max_row_nodes) *max_row_nodes = P->max_deg;
+    return SA_OK;
+}
+
+int sa_plan_stats(const sa_plan *P, int64_t *out, int n)
+{
+    if (!P || !out) return set_error(SA_ERR_ARG, "plan/out is NULL");
+    const int64_t v[8] = {P->n_templates, P->tm_ok ? 1 : 0, P->fold_ok ? 1 : 0, P->n_inc,
+                          P->tm_nwords, P->max_deg, P->nnodes, P->nnz};
+    for (int i = 0; i < n && i < 8; ++i) out[i] = v[i];
     return SA_OK;
 }
 
@@ -790,12 +1455,18 @@ int sa_numeric(sa_plan *P, int ops, const sa_coeffs *cf, double *const *vals_dev
     const double den = (double)((d + 1) * (d + 2) * (d + 3));
     a.mass_coef_diag = 2.0 / den;
     a.mass_coef_off = 1.0 / den;
+    {
+        // ((W0 + W1) + ... + Wd) + W[alpha]) + W[beta] with every W = w_const
+        double ws = a.w_const;
+        for (int k = 1; k <= d; ++k) ws = ws + a.w_const;
+        a.mass_wc = (ws + a.w_const) + a.w_const;
+    }
     SA_CUDA_TRY(cudaMemsetAsync(P->counters, 0, 4 * sizeof(int64_t), st));
     SA_CUDA_TRY(cudaMemsetAsync(P->counters + 4, 0x7f, sizeof(int64_t), st));
     int rc;
-    if (d == 1) rc = dispatch_numeric<1>(a, ops, P->m, P->nnodes, M->core, st);
-    else if (d == 2) rc = dispatch_numeric<2>(a, ops, P->m, P->nnodes, M->core, st);
-    else rc = dispatch_numeric<3>(a, ops, P->m, P->nnodes, M->core, st);
+    if (d == 1) rc = sa_dispatch_d1(P, a, ops, M->core, st);
+    else if (d == 2) rc = sa_dispatch_d2(P, a, ops, M->core, st);
+    else rc = sa_dispatch_d3(P, a, ops, M->core, st);
     if (rc != SA_OK) return rc;
     if (n_zero_out) {
         int64_t h[5];
@@ -828,3 +1499,4 @@ int sa_compact(const sa_plan *P, const double *vals_dev, int64_t *indptr_out, in
 }
 
 }  // extern "C"
+#endif  // SA_ABI

@@ -145,6 +145,13 @@ class Plan:
     def handle(self):
         return self._h
 
+    def stats(self) -> dict:
+        out = (ctypes.c_int64 * 8)()
+        _lib.check(_lib.load().sa_plan_stats(self._h, out, 8))
+        keys = ("templates", "templates_ok", "fold_ok", "incidences", "template_words", "max_row_nodes",
+                "nodes", "nnz")
+        return dict(zip(keys, [int(x) for x in out]))
+
     def pattern(self, stream=None):
         """Structural (indptr int64 relative, indices int32) of the block."""
         if self._pattern is None:

@@ -169,3 +169,68 @@ def test_full_size_c2_properties(cuda_ok):
     rows = np.repeat(np.arange(stiff.nrows), np.diff(stiff.row_ptr))
     rs = np.bincount(rows, weights=stiff.vals, minlength=stiff.nrows)
     assert np.max(np.abs(rs)) < 1e-9                    # constants are in the kernel
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_golden_bitwise_tile_kernel(cuda_ok, name, monkeypatch):
+    # the tile kernel (templates + per-tile element dedupe) is bitwise too
+    monkeypatch.setenv("SA_KERNEL", "tile")
+    g = load_golden(name)
+    mesh = golden_mesh(g)
+    k = device_kernel_for(name, g, mesh)
+    got = P.assemble_vector_b200(mesh, k) if k.m > 1 else P.assemble_b200(mesh, k)
+    assert_csr_equal(got, g["row_ptr"], g["col_idx"], g["vals"])
+
+
+def test_structured_mesh_uses_few_templates(cuda_ok, monkeypatch):
+    from paper_1401_3301_b200.device import DeviceMesh
+
+    monkeypatch.setenv("SA_KERNEL", "tile")
+    mesh = _jittered(3, 12, 5)
+    st = DeviceMesh(mesh.q, mesh.me, mesh.vols).plan(1).stats()
+    # 1729 nodes in 217 tiles collapse to a few dozen distinct templates
+    assert st["templates_ok"] == 1 and st["templates"] <= 100, st
+
+
+@pytest.mark.parametrize("kernel", ["rowgather", "tile"])
+def test_unstructured_delaunay_mesh(cuda_ok, kernel, monkeypatch):
+    # random points, Delaunay triangulation: rows have (mostly) distinct templates
+    monkeypatch.setenv("SA_KERNEL", kernel)
+    from scipy.spatial import Delaunay
+
+    from paper_1401_3301_b200.device import DeviceMesh
+    from oracle import oracle as O
+
+    for d, npts in ((2, 4000), (3, 1500)):
+        rng = np.random.default_rng(d)
+        pts = rng.random((npts, d))
+        tri = Delaunay(pts)
+        q = np.ascontiguousarray(pts.T)
+        me = np.ascontiguousarray(tri.simplices.T.astype(np.int64))
+        try:
+            vols = O.volumes(q, me)
+        except O.OracleDegenerate:
+            continue
+        keep = vols > 1e-10
+        me = np.ascontiguousarray(me[:, keep])
+        mesh = P.Mesh(q, me, O.volumes(q, me))
+        st = DeviceMesh(mesh.q, mesh.me, mesh.vols).plan(1).stats()
+        if kernel == "tile":  # unstructured: (almost) every tile has its own template
+            assert st["templates"] > 20 and st["templates_ok"] == 1, st
+        mass, stiff = P.assemble_many_b200(mesh, [P.MassKernel(mesh, 1.0 + mesh.q[0]), P.StiffnessKernel(mesh)])
+        assert_csr_equal(stiff, *_oracle(mesh, "stiffness", nthreads=4))
+        assert_csr_equal(mass, *_oracle(mesh, "mass", nthreads=4, w=1.0 + mesh.q[0]))
+
+
+@pytest.mark.parametrize("k", [40, 70])
+def test_high_valence_node(cuda_ok, k):
+    # a fan of k triangles around node 0: 40 incidences stays on the tile
+    # kernel (<= 64), 70 routes the plan to the row-gather kernel
+    from oracle import oracle as O
+
+    ang = np.linspace(0, 2 * np.pi, k, endpoint=False)
+    q = np.vstack([np.concatenate([[0.0], np.cos(ang)]), np.concatenate([[0.0], np.sin(ang)])])
+    me = np.array([[0] * k, [1 + i for i in range(k)], [1 + (i + 1) % k for i in range(k)]])
+    mesh = P.Mesh(q, me, O.volumes(q, me))
+    got = P.assemble_b200(mesh, P.StiffnessKernel(mesh))
+    assert_csr_equal(got, *_oracle(mesh, "stiffness", nthreads=1))
