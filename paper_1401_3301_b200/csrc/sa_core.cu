@@ -296,7 +296,9 @@ __global__ void k_fold_lists(const int64_t *__restrict__ inc_ptr, const uint2 *_
 //                           element per row): 4 x 16-bit fold positions,
 //                           one per local column beta
 //   w[PB .. PB+nrows)       per row: deg | entb << 16
-//   w[OB .. )               NE+1 uint16 entry offsets into the fold array
+//   w[OB .. OB+(NE+2)/2)    NE+1 uint16 entry offsets into the fold array
+//   w[LB .. LB+17)          33 uint16: lane l sums entries [ls[l], ls[l+1]),
+//                           split so every lane gets ~1/32 of the contributions
 // The fold array of a tile is entry-major: entry k's contributions occupy
 // [off[k], off[k+1]) in ascending element order.  Element lanes scatter their
 // local rows straight into it; row lanes then sum contiguous runs.
@@ -313,7 +315,7 @@ constexpr int TILE_MAX_ELEM = 255;
 
 __host__ __device__ inline int64_t tile_stride_bound(int64_t NI, int64_t NE, int64_t R)
 {
-    return 2 + 2 * (NI < TILE_MAX_ELEM ? NI : TILE_MAX_ELEM) + 2 * NI + R + (NE + 2) / 2 + 4;
+    return 2 + 2 * (NI < TILE_MAX_ELEM ? NI : TILE_MAX_ELEM) + 2 * NI + R + (NE + 2) / 2 + 17 + 4;
 }
 
 template <int D>
@@ -359,8 +361,8 @@ __global__ void k_tile_build(const int64_t *__restrict__ inc_ptr, const uint32_t
         uint32_t &sw = w[2 + ne + lo];
         sw = (sw & ~(0xffu << (8 * alpha))) | ((uint32_t)i << (8 * alpha));
     }
-    const uint32_t SB = 2 + 2 * ne, PB = SB + 2 * NI, OB = PB + nr;
-    const uint32_t end = OB + ((NE + 2) >> 1);
+    const uint32_t SB = 2 + 2 * ne, PB = SB + 2 * NI, OB = PB + nr, LB = OB + ((NE + 2) >> 1);
+    const uint32_t end = LB + 17;
     for (uint32_t x = SB; x < end; ++x) w[x] = 0;
     for (int row = 0; row < nr; ++row) {
         const int64_t ip = inc_ptr[r0 + row];
@@ -380,6 +382,17 @@ __global__ void k_tile_build(const int64_t *__restrict__ inc_ptr, const uint32_t
                 const uint32_t kg = entb + k;
                 w[OB + (kg >> 1)] |= (pos + 1) << (16 * (kg & 1));
             }
+        }
+    }
+    // lane starts: lane l takes the entries whose runs start in [l*NC/32, (l+1)*NC/32)
+    {
+        const uint32_t NC = (uint32_t)((D + 1) * NI);
+        int k = 0;
+        for (int l = 0; l <= 32; ++l) {
+            const uint32_t target = (uint32_t)(((uint64_t)NC * l) / 32);
+            while (k < NE && ((w[OB + (k >> 1)] >> (16 * (k & 1))) & 0xffff) < target) ++k;
+            const uint32_t v = l == 32 ? (uint32_t)NE : (uint32_t)k;
+            w[LB + (l >> 1)] |= v << (16 * (l & 1));
         }
     }
     words_out[T] = end;
@@ -841,37 +854,34 @@ __global__ void __launch_bounds__(128) k_numeric_tiles(NumArgs a, TileArgs t)
     for (int o = 0; o < NOUT; ++o) nz[o] = 0;
     const int64_t base = a.indptr[(int64_t)M * r0];
     if constexpr (M == 1) {
-        // phase 2 (scalar): lanes over the tile's entries, which are in CSR
-        // order; a warp-uniform loop over contribution ranks (predicated, no
-        // divergent branches) sums each entry's contiguous run left to right,
-        // and the result is stored straight to its CSR position (coalesced).
-        for (int k0 = 0; k0 < NE; k0 += 32) {
-            const int kg = k0 + lane;
-            const bool valid = kg < NE;
-            unsigned s0 = 0, s1 = 0;
-            if (valid) {
-                s0 = (__ldg(t.tm + OB + (kg >> 1)) >> (16 * (kg & 1))) & 0xffff;
-                s1 = (__ldg(t.tm + OB + ((kg + 1) >> 1)) >> (16 * ((kg + 1) & 1))) & 0xffff;
-            }
-            const int cnt = (int)(s1 - s0);
-            const int maxc = __reduce_max_sync(0xffffffffu, cnt);
+        // phase 2 (scalar): the tile's entries are in CSR order and their runs
+        // are contiguous in the fold array; lane l sums the entries whose runs
+        // start in its 1/32 of the contributions (balanced, no carries: each
+        // run is summed left to right by one lane) and stores each result to
+        // its CSR position.
+        const unsigned LB = OB + ((NE + 2) >> 1);
+        const int kb = (__ldg(t.tm + LB + (lane >> 1)) >> (16 * (lane & 1))) & 0xffff;
+        const int ke = (__ldg(t.tm + LB + ((lane + 1) >> 1)) >> (16 * ((lane + 1) & 1))) & 0xffff;
+        if (kb < ke) {
+            auto off = [&](int k) { return (int)((__ldg(t.tm + OB + (k >> 1)) >> (16 * (k & 1))) & 0xffff); };
+            int k = kb;
+            int s = off(kb), next = off(kb + 1);
+            const int se = off(ke);
             double acc[NOUT];
 #pragma unroll
             for (int o = 0; o < NOUT; ++o) acc[o] = 0.0;
-            for (int i = 0; i < maxc; ++i) {
-                const bool on = i < cnt;
-                const unsigned sidx = on ? s0 + i : 0;
+            for (; s < se; ++s) {
 #pragma unroll
-                for (int o = 0; o < NOUT; ++o) {
-                    const double v = F[o * FS + sidx];
-                    acc[o] = on ? SA_ADD(acc[o], v) : acc[o];
-                }
-            }
-            if (valid) {
+                for (int o = 0; o < NOUT; ++o) acc[o] = SA_ADD(acc[o], F[o * FS + s]);
+                if (s + 1 == next) {
 #pragma unroll
-                for (int o = 0; o < NOUT; ++o) {
-                    a.vals[o][base + kg] = acc[o];
-                    nz[o] += (acc[o] == 0.0);
+                    for (int o = 0; o < NOUT; ++o) {
+                        a.vals[o][base + k] = acc[o];
+                        nz[o] += (acc[o] == 0.0);
+                        acc[o] = 0.0;
+                    }
+                    ++k;
+                    if (k < ke) next = off(k + 1);
                 }
             }
         }

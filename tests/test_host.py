@@ -98,3 +98,25 @@ def test_error_mapping():
         _lib.check(_lib.SA_ERR_ARG)
     with pytest.raises(CapacityError):
         _lib.check(_lib.SA_ERR_CAPACITY)
+
+
+def test_register_into_reference_registries():
+    # the drop-in: variant "b200" appears in the reference's own registries
+    import importlib
+    import sys
+
+    ref = "/root/reference/pkg/src"
+    if not os.path.isdir(ref):
+        pytest.skip("reference tree not present (GPU box)")
+    sys.path.insert(0, ref)
+    try:
+        ra = importlib.import_module("simplex_asm.assembly")
+        rb = importlib.import_module("simplex_asm.bench")
+        from paper_1401_3301_b200 import assembly
+
+        assert assembly.register()
+        assert ra.SCALAR_DRIVERS["b200"] is assembly.assemble_b200
+        assert ra.VECTOR_DRIVERS["b200"] is assembly.assemble_vector_b200
+        assert "b200" in rb.VARIANTS_FOR["stiffness"] and "b200" in rb.VARIANTS_FOR["elastic"]
+    finally:
+        sys.path.remove(ref)
