@@ -319,6 +319,7 @@ def main():
         "config": {"workload": args.config, **config_desc(cfg), "nq": nq, "nme": nme,
                    "nnz_structural_per_matrix": nnz_struct_all, "n_out": len(kernels),
                    "exact_zero_entries": zeros, "parallelism": f"row-blocks x{world}",
+                   "plan": plan.stats(), "kernel": os.environ.get("SA_KERNEL", "default"),
                    "l2": "flushed between timed steps (256 MiB write); inputs+outputs > L2",
                    "timing": "per-step CUDA events on the launching stream, summed; max over ranks"},
         "nnz_per_s": nnz_struct_all * len(kernels) / (ms_per_step * 1e-3),

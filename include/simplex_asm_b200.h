@@ -83,8 +83,9 @@ int sa_plan_info(const sa_plan *plan, int64_t *nrows, int64_t *nnz_structural,
 /* Structural CSR of the block (indptr relative, int64 (nrows+1); indices
  * global column dofs int32 (nnz)), into caller-allocated device buffers. */
 int sa_plan_pattern(const sa_plan *plan, int64_t *indptr_dev, int32_t *indices_dev, void *stream);
-/* Diagnostics: out[0..n) = {fold templates, templates verified, all nodes
- * <= 32 incidences, incidences, template words, max row nodes, nodes, nnz}. */
+/* Diagnostics: out[0..n) = {tile templates, tile templates verified, every
+ * node <= 64 incidences, incidences, tile template words, max row nodes,
+ * nodes, nnz, chunk plan ok, chunks, chunk templates, chunk template words}. */
 int sa_plan_stats(const sa_plan *plan, int64_t *out, int n);
 int sa_plan_destroy(sa_plan *plan);
 

@@ -19,6 +19,7 @@
 
 #include "sa_common.cuh"
 #include "sa_geometry.cuh"
+#include "sa_radix.cuh"
 
 using namespace sa;
 
@@ -59,6 +60,17 @@ struct sa_plan {
     // per tile size R = 2^c (c = 0..5): max incidences / node-level entries in one tile of R rows
     int64_t tile_max_inc[6] = {0, 0, 0, 0, 0, 0};
     int64_t tile_max_ent[6] = {0, 0, 0, 0, 0, 0};
+    // chunk kernel
+    bool ck_ok = false;
+    unsigned ck_emin = 0, ck_emax = 0;
+    int ck_C = 0;
+    int64_t ck_nchunks = 0, ck_ntemplates = 0, ck_nwords = 0;
+    uint32_t *ck_tm = nullptr, *ck_pb = nullptr, *ck_tm_off = nullptr, *ck_tmw = nullptr;
+    unsigned *ck_flags = nullptr;  // nrec record flags + 1 ticket
+    uint32_t *ck_rs = nullptr;     // first record index per chunk
+    int64_t ck_nrec = 0;
+    int64_t ck_maxw = 0;           // largest chunk template (words)
+    unsigned ck_epoch = 0;         // bumped per launch
 };
 
 // numeric-phase arguments (shared by the per-dimension translation units)
@@ -786,6 +798,13 @@ inline bool want_tile_kernel()
     const char *k = getenv("SA_KERNEL");
     return k && strcmp(k, "tile") == 0;
 }
+// SA_KERNEL=chunk selects the element-chunk kernel (its symbolic data is then
+// built); the row-gather kernel is the default (fastest measured, profiles/)
+inline bool want_chunk_kernel()
+{
+    const char *k = getenv("SA_KERNEL");
+    return k && strcmp(k, "chunk") == 0;
+}
 
 // lanes per row (R = 32/L rows per warp tile): default per (d, m), override
 // with SA_TILE_LANES at plan creation (tuning).
@@ -934,6 +953,8 @@ __global__ void __launch_bounds__(128) k_numeric_tiles(NumArgs a, TileArgs t)
     }
 }
 
+#include "sa_chunk.cuh"
+
 // compaction (K5): drop exact-zero entries (sparse.py:108-111)
 __global__ void k_row_nonzeros(const int64_t *__restrict__ indptr, const double *__restrict__ vals, int64_t nrows,
                                int64_t *__restrict__ cnt)
@@ -1078,6 +1099,180 @@ int build_tile_templates(sa_plan *P, int R, cudaStream_t st)
     return rc;
 }
 
+// Host side of the chunk kernel's symbolic data (see sa_chunk.cuh).
+template <int D>
+int build_chunks(sa_plan *P, cudaStream_t st)
+{
+    const int64_t nn = P->nnodes;
+    if (!nn || !P->n_inc) return SA_OK;
+    unsigned *mm = nullptr;
+    SA_CUDA_TRY(cudaMallocAsync((void **)&mm, 2 * sizeof(unsigned), st));
+    const unsigned init[2] = {0xffffffffu, 0u};
+    SA_CUDA_TRY(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, st));
+    SA_LAUNCH(k_inc_minmax<D>, std::min<int64_t>(grid_for(P->n_inc, 256), 148 * 8), 256, 0, st, P->inc_e, P->n_inc, mm);
+    unsigned hmm[2];
+    SA_CUDA_TRY(cudaMemcpyAsync(hmm, mm, sizeof hmm, cudaMemcpyDeviceToHost, st));
+    SA_CUDA_TRY(cudaStreamSynchronize(st));
+    SA_CUDA_TRY(cudaFreeAsync(mm, st));
+    const int C = chunk_elems(D, P->m);
+    const int64_t nchunks = ((int64_t)hmm[1] - hmm[0]) / C + 1;
+    P->ck_emin = hmm[0];
+    P->ck_emax = hmm[1];
+    P->ck_C = C;
+    P->ck_nchunks = nchunks;
+
+    // records: count, scan, fill
+    int64_t *rcount = nullptr, *rstart = nullptr;
+    SA_CUDA_TRY(cudaMallocAsync((void **)&rcount, (nn + 1) * sizeof(int64_t), st));
+    SA_CUDA_TRY(cudaMallocAsync((void **)&rstart, (nn + 1) * sizeof(int64_t), st));
+    SA_LAUNCH(k_chunk_records<D>, grid_for(nn, 128), 128, 0, st, P->inc_ptr, P->inc_e, P->fold, P->colptr, P->indptr,
+              nn, P->m, hmm[0], C, rcount, (const int64_t *)nullptr, (uint64_t *)nullptr, (uint32_t *)nullptr,
+              (uint32_t *)nullptr, (uint32_t *)nullptr, (uint32_t *)nullptr, (uint32_t *)nullptr, (uint16_t *)nullptr);
+    SA_TRY(exclusive_scan_i64(rcount, rstart, nn, P->scan_tmp, st));
+    int64_t nrec = 0;
+    SA_CUDA_TRY(cudaMemcpyAsync(&nrec, rstart + nn, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SA_CUDA_TRY(cudaStreamSynchronize(st));
+    if (nrec >= ((int64_t)1 << 32)) {
+        SA_CUDA_TRY(cudaFreeAsync(rcount, st));
+        SA_CUDA_TRY(cudaFreeAsync(rstart, st));
+        return SA_OK;
+    }
+    uint64_t *k0 = nullptr, *k1 = nullptr;
+    uint32_t *v0 = nullptr, *v1 = nullptr, *rp = nullptr, *rmeta = nullptr, *rprev = nullptr, *rcoff = nullptr;
+    uint16_t *contrib = nullptr;
+    const int64_t nr1 = std::max<int64_t>(nrec, 1);
+    SA_CUDA_TRY(cudaMallocAsync((void **)&k0, nr1 * sizeof(uint64_t), st));
+    SA_CUDA_TRY(cudaMallocAsync((void **)&k1, nr1 * sizeof(uint64_t), st));
+    SA_CUDA_TRY(cudaMallocAsync((void **)&v0, nr1 * sizeof(uint32_t), st));
+    SA_CUDA_TRY(cudaMallocAsync((void **)&v1, nr1 * sizeof(uint32_t), st));
+    SA_CUDA_TRY(cudaMallocAsync((void **)&rp, nr1 * sizeof(uint32_t), st));
+    SA_CUDA_TRY(cudaMallocAsync((void **)&rmeta, nr1 * sizeof(uint32_t), st));
+    SA_CUDA_TRY(cudaMallocAsync((void **)&rprev, nr1 * sizeof(uint32_t), st));
+    SA_CUDA_TRY(cudaMallocAsync((void **)&rcoff, nr1 * sizeof(uint32_t), st));
+    SA_CUDA_TRY(cudaMallocAsync((void **)&contrib, (D + 1) * P->n_inc * sizeof(uint16_t), st));
+    SA_LAUNCH(k_chunk_records<D>, grid_for(nn, 128), 128, 0, st, P->inc_ptr, P->inc_e, P->fold, P->colptr, P->indptr,
+              nn, P->m, hmm[0], C, (int64_t *)nullptr, (const int64_t *)rstart, k0, v0, rp, rmeta, rprev, rcoff,
+              contrib);
+    int kbits = 0;
+    while (((int64_t)1 << kbits) < nchunks) ++kbits;
+    int which = 0;
+    SA_TRY(radix::sort_pairs(k0, v0, k1, v1, nrec, std::max(8, (kbits + 7) & ~7), st, &which));
+    const uint64_t *skey = which ? k1 : k0;
+    const uint32_t *order = which ? v1 : v0;
+    int64_t *cstart = nullptr;
+    SA_CUDA_TRY(cudaMallocAsync((void **)&cstart, (nchunks + 1) * sizeof(int64_t), st));
+    SA_LAUNCH(k_chunk_bounds, grid_for(nrec, 256), 256, 0, st, skey, nrec, nchunks, cstart);
+    std::vector<int64_t> hcs(nchunks + 1);
+    SA_CUDA_TRY(cudaMemcpyAsync(hcs.data(), cstart, (nchunks + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SA_CUDA_TRY(cudaStreamSynchronize(st));
+    int64_t maxrec = 0;
+    for (int64_t k = 0; k < nchunks; ++k) maxrec = std::max(maxrec, hcs[k + 1] - hcs[k]);
+    const int64_t stride = 2 + 5 * maxrec + (int64_t)C * (D + 1) * (D + 1) / 2 + 8;
+    uint32_t *inv = nullptr;
+    SA_CUDA_TRY(cudaMallocAsync((void **)&inv, nr1 * sizeof(uint32_t), st));
+    SA_LAUNCH(k_inverse, grid_for(nrec, 256), 256, 0, st, order, nrec, inv);
+    uint32_t *fpos = nullptr;
+    SA_CUDA_TRY(cudaMallocAsync((void **)&fpos, nr1 * sizeof(uint32_t), st));
+    SA_LAUNCH(k_chunk_order, grid_for(nchunks, 128), 128, 0, st, (const int64_t *)cstart, nchunks, order, rmeta, fpos);
+
+    // templates, built and deduplicated in batches of chunks (bounded scratch)
+    SA_CUDA_TRY(cudaMallocAsync((void **)&P->ck_tm, nchunks * sizeof(uint32_t), st));
+    SA_CUDA_TRY(cudaMallocAsync((void **)&P->ck_pb, nchunks * sizeof(uint32_t), st));
+    const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(nchunks, ((int64_t)1 << 29) / (stride * 4)));
+    uint32_t *scratch = nullptr, *words = nullptr;
+    uint64_t *sig = nullptr;
+    SA_CUDA_TRY(cudaMallocAsync((void **)&scratch, batch * stride * sizeof(uint32_t), st));
+    SA_CUDA_TRY(cudaMallocAsync((void **)&words, batch * sizeof(uint32_t), st));
+    SA_CUDA_TRY(cudaMallocAsync((void **)&sig, batch * sizeof(uint64_t), st));
+    std::unordered_map<uint64_t, uint32_t> ids;
+    std::vector<uint32_t> tm_off_h;
+    std::vector<uint32_t> tm_h;        // packed template words (host copy)
+    std::vector<uint32_t> ctm(nchunks);
+    std::vector<uint64_t> hs(batch);
+    std::vector<uint32_t> hw(batch);
+    bool ok = true;
+    for (int64_t b0 = 0; b0 < nchunks && ok; b0 += batch) {
+        const int64_t nb = std::min(batch, nchunks - b0);
+        SA_CUDA_TRY(cudaMemsetAsync(P->counters + 6, 0, sizeof(int64_t), st));
+        SA_LAUNCH(k_chunk_build, grid_for(nb, 64), 64, 0, st, (const int64_t *)cstart, b0, nb, order, inv, skey, rp,
+                  rmeta, rcoff, contrib, (const uint32_t *)fpos, stride, scratch, words, sig, P->ck_pb + b0,
+                  (unsigned long long *)(P->counters + 6));
+        int64_t fail = 0;
+        SA_CUDA_TRY(cudaMemcpyAsync(hs.data(), sig, nb * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        SA_CUDA_TRY(cudaMemcpyAsync(hw.data(), words, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        SA_CUDA_TRY(cudaMemcpyAsync(&fail, P->counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        if (fail) { ok = false; break; }
+        // new templates of this batch: copy their words back (small for structured meshes)
+        std::vector<int64_t> fresh;
+        for (int64_t i = 0; i < nb; ++i) {
+            auto it = ids.find(hs[i]);
+            if (it == ids.end()) {
+                const uint32_t id = (uint32_t)tm_off_h.size();
+                ids.emplace(hs[i], id);
+                tm_off_h.push_back((uint32_t)tm_h.size());
+                const size_t at = tm_h.size();
+                tm_h.resize(at + hw[i]);
+                SA_CUDA_TRY(cudaMemcpyAsync(tm_h.data() + at, scratch + i * stride, hw[i] * sizeof(uint32_t),
+                                            cudaMemcpyDeviceToHost, st));
+                ctm[b0 + i] = id;
+            } else {
+                ctm[b0 + i] = it->second;
+            }
+        }
+        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        // exact verification of this batch against the templates so far
+        if (tm_h.size() >= ((size_t)1 << 31)) { ok = false; break; }
+        uint32_t *dtm = nullptr, *doff = nullptr, *dctm = nullptr;
+        SA_CUDA_TRY(cudaMallocAsync((void **)&dtm, std::max<size_t>(tm_h.size(), 1) * sizeof(uint32_t), st));
+        SA_CUDA_TRY(cudaMallocAsync((void **)&doff, tm_off_h.size() * sizeof(uint32_t), st));
+        SA_CUDA_TRY(cudaMallocAsync((void **)&dctm, nb * sizeof(uint32_t), st));
+        SA_CUDA_TRY(cudaMemcpyAsync(dtm, tm_h.data(), tm_h.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+        SA_CUDA_TRY(cudaMemcpyAsync(doff, tm_off_h.data(), tm_off_h.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+        SA_CUDA_TRY(cudaMemcpyAsync(dctm, ctm.data() + b0, nb * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+        SA_CUDA_TRY(cudaMemsetAsync(P->counters + 6, 0, sizeof(int64_t), st));
+        SA_LAUNCH(k_tile_verify, grid_for(nb * 32, 128), 128, 0, st, scratch, (int)stride, words, nb, dctm, doff, dtm,
+                  (unsigned long long *)(P->counters + 6));
+        int64_t bad = 0;
+        SA_CUDA_TRY(cudaMemcpyAsync(&bad, P->counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        SA_CUDA_TRY(cudaFreeAsync(dtm, st));
+        SA_CUDA_TRY(cudaFreeAsync(doff, st));
+        SA_CUDA_TRY(cudaFreeAsync(dctm, st));
+        if (bad) ok = false;
+    }
+    if (ok) {
+        for (size_t t = 0; t < tm_off_h.size(); ++t) {
+            const size_t end = t + 1 < tm_off_h.size() ? tm_off_h[t + 1] : tm_h.size();
+            P->ck_maxw = std::max<int64_t>(P->ck_maxw, (int64_t)(end - tm_off_h[t]));
+        }
+        tm_off_h.push_back((uint32_t)tm_h.size());   // sentinel: template t spans [off[t], off[t+1])
+        P->ck_ntemplates = (int64_t)tm_off_h.size() - 1;
+        P->ck_nwords = (int64_t)tm_h.size();
+        SA_CUDA_TRY(cudaMallocAsync((void **)&P->ck_tm_off, std::max<size_t>(tm_off_h.size(), 1) * sizeof(uint32_t), st));
+        SA_CUDA_TRY(cudaMallocAsync((void **)&P->ck_tmw, std::max<size_t>(tm_h.size(), 1) * sizeof(uint32_t), st));
+        SA_CUDA_TRY(cudaMallocAsync((void **)&P->ck_flags, (nrec + 1) * sizeof(unsigned), st));
+        SA_CUDA_TRY(cudaMemsetAsync(P->ck_flags, 0, (nrec + 1) * sizeof(unsigned), st));
+        std::vector<uint32_t> rs(nchunks);
+        for (int64_t k = 0; k < nchunks; ++k) rs[k] = (uint32_t)hcs[k];
+        SA_CUDA_TRY(cudaMallocAsync((void **)&P->ck_rs, nchunks * sizeof(uint32_t), st));
+        SA_CUDA_TRY(cudaMemcpyAsync(P->ck_rs, rs.data(), nchunks * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+        P->ck_nrec = nrec;
+        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        SA_CUDA_TRY(cudaMemcpyAsync(P->ck_tm_off, tm_off_h.data(), tm_off_h.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+        SA_CUDA_TRY(cudaMemcpyAsync(P->ck_tmw, tm_h.data(), tm_h.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+        SA_CUDA_TRY(cudaMemcpyAsync(P->ck_tm, ctm.data(), nchunks * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    }
+    SA_CUDA_TRY(cudaStreamSynchronize(st));
+    for (void *p : {(void *)rcount, (void *)rstart, (void *)k0, (void *)k1, (void *)v0, (void *)v1, (void *)rp,
+                    (void *)rmeta, (void *)rprev, (void *)rcoff, (void *)contrib, (void *)cstart, (void *)scratch,
+                    (void *)words, (void *)sig, (void *)inv, (void *)fpos})
+        SA_CUDA_TRY(cudaFreeAsync(p, st));
+    SA_CUDA_TRY(cudaStreamSynchronize(st));
+    P->ck_ok = ok;
+    return SA_OK;
+}
+
 template <int D>
 int symbolic_kernels(sa_plan *P, cudaStream_t st)
 {
@@ -1167,6 +1362,7 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
     SA_LAUNCH(k_dof_csr, grid_for(nn + 1, 128), 128, 0, st, P->colptr, P->cols, nn, m, P->indptr, P->indices);
     SA_CUDA_TRY(cudaFreeAsync(cnt, st));
     SA_CUDA_TRY(cudaStreamSynchronize(st));
+    if (P->fold_ok && want_chunk_kernel()) SA_TRY(build_chunks<D>(P, st));
     return SA_OK;
 }
 
@@ -1221,8 +1417,44 @@ int launch_tiles(const sa_plan *P, const NumArgs &a, cudaStream_t st)
 }
 
 template <int D, int M, int OPS, int CORE>
+int launch_chunks(const sa_plan *P, const NumArgs &a, cudaStream_t st)
+{
+    constexpr int NOUT = n_outputs<OPS>();
+    constexpr int VPE = NOUT * M * M * (D + 1) * (D + 1);
+    const size_t smem = (size_t)P->ck_C * VPE * sizeof(double) + (size_t)P->ck_maxw * sizeof(uint32_t);
+    if (smem > 200 * 1024) return 1000;
+    auto kern = k_numeric_chunks<D, M, OPS, CORE>;
+    SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0, nsm = 148, occ = 1;
+    SA_CUDA_TRY(cudaGetDevice(&dev));
+    SA_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const int threads = std::max(64, std::min(256, P->ck_C));
+    SA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+    ChunkArgs c;
+    c.chunk_tm = P->ck_tm;
+    c.chunk_pb = P->ck_pb;
+    c.tm_off = P->ck_tm_off;
+    c.tm = P->ck_tmw;
+    c.chunk_rs = P->ck_rs;
+    c.rflags = P->ck_flags;
+    c.ticket = P->ck_flags + P->ck_nrec;
+    c.epoch = ++const_cast<sa_plan *>(P)->ck_epoch;
+    c.nowait = getenv("SA_CHUNK_NOWAIT") != nullptr;
+    c.max_words = (int)P->ck_maxw;
+    c.nchunks = P->ck_nchunks;
+    c.emin = P->ck_emin;
+    c.emax = P->ck_emax;
+    c.C = P->ck_C;
+    SA_CUDA_TRY(cudaMemsetAsync(c.ticket, 0, sizeof(unsigned), st));
+    const int64_t grid = std::min<int64_t>(P->ck_nchunks, (int64_t)nsm * std::max(occ, 1));
+    if (grid > 0) SA_LAUNCH(kern, (unsigned)grid, threads, smem, st, a, c);
+    return SA_OK;
+}
+
+template <int D, int M, int OPS, int CORE>
 int launch_numeric(const sa_plan *P, const NumArgs &a, cudaStream_t st)
 {
+    if (P->ck_ok && want_chunk_kernel()) SA_TRY_OR_FALL(launch_chunks<D, M, OPS, CORE>(P, a, st));
     const int64_t nnodes = P->nnodes;
     const bool use_tile = P->tm_ok && want_tile_kernel();
     if (use_tile) {
@@ -1366,6 +1598,8 @@ int sa_plan_destroy(sa_plan *P)
     cudaFree(P->indptr); cudaFree(P->indices); cudaFree(P->counters); cudaFree(P->scan_tmp);
     cudaFree(P->inc_e); cudaFree(P->fold);
     cudaFree(P->tile_e0); cudaFree(P->tile_tm); cudaFree(P->tm_off); cudaFree(P->tm);
+    cudaFree(P->ck_tm); cudaFree(P->ck_pb); cudaFree(P->ck_tm_off); cudaFree(P->ck_tmw); cudaFree(P->ck_flags);
+    cudaFree(P->ck_rs);
     delete P;
     return SA_OK;
 }
@@ -1417,9 +1651,10 @@ int sa_plan_info(const sa_plan *P, int64_t *nrows, int64_t *nnz, int64_t *max_ro
 int sa_plan_stats(const sa_plan *P, int64_t *out, int n)
 {
     if (!P || !out) return set_error(SA_ERR_ARG, "plan/out is NULL");
-    const int64_t v[8] = {P->n_templates, P->tm_ok ? 1 : 0, P->fold_ok ? 1 : 0, P->n_inc,
-                          P->tm_nwords, P->max_deg, P->nnodes, P->nnz};
-    for (int i = 0; i < n && i < 8; ++i) out[i] = v[i];
+    const int64_t v[12] = {P->n_templates, P->tm_ok ? 1 : 0, P->fold_ok ? 1 : 0, P->n_inc,
+                           P->tm_nwords, P->max_deg, P->nnodes, P->nnz,
+                           P->ck_ok ? 1 : 0, P->ck_nchunks, P->ck_ntemplates, P->ck_nwords};
+    for (int i = 0; i < n && i < 12; ++i) out[i] = v[i];
     return SA_OK;
 }
 
@@ -1473,15 +1708,17 @@ int sa_numeric(sa_plan *P, int ops, const sa_coeffs *cf, double *const *vals_dev
     }
     SA_CUDA_TRY(cudaMemsetAsync(P->counters, 0, 4 * sizeof(int64_t), st));
     SA_CUDA_TRY(cudaMemsetAsync(P->counters + 4, 0x7f, sizeof(int64_t), st));
+    SA_CUDA_TRY(cudaMemsetAsync(P->counters + 7, 0, sizeof(int64_t), st));
     int rc;
     if (d == 1) rc = sa_dispatch_d1(P, a, ops, M->core, st);
     else if (d == 2) rc = sa_dispatch_d2(P, a, ops, M->core, st);
     else rc = sa_dispatch_d3(P, a, ops, M->core, st);
     if (rc != SA_OK) return rc;
     if (n_zero_out) {
-        int64_t h[5];
-        SA_CUDA_TRY(cudaMemcpyAsync(h, P->counters, 5 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        int64_t h[8];
+        SA_CUDA_TRY(cudaMemcpyAsync(h, P->counters, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
         SA_CUDA_TRY(cudaStreamSynchronize(st));
+        if (h[7]) return set_error(SA_ERR_CUDA, "chunk kernel: a carry wait timed out (internal error)");
         for (int o = 0; o < nout; ++o) n_zero_out[o] = h[o];
         if (h[4] != 0x7f7f7f7f7f7f7f7fLL) {
             err_state().bad = h[4];

@@ -146,10 +146,10 @@ class Plan:
         return self._h
 
     def stats(self) -> dict:
-        out = (ctypes.c_int64 * 8)()
-        _lib.check(_lib.load().sa_plan_stats(self._h, out, 8))
+        out = (ctypes.c_int64 * 12)()
+        _lib.check(_lib.load().sa_plan_stats(self._h, out, 12))
         keys = ("templates", "templates_ok", "fold_ok", "incidences", "template_words", "max_row_nodes",
-                "nodes", "nnz")
+                "nodes", "nnz", "chunk_ok", "chunks", "chunk_templates", "chunk_template_words")
         return dict(zip(keys, [int(x) for x in out]))
 
     def pattern(self, stream=None):
