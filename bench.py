@@ -327,7 +327,8 @@ def main():
         "numeric_ms": ms_per_step,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                     "algorithmic_bytes": b_num, "kernel": "k_numeric_tile",
+                     "algorithmic_bytes": b_num, "kernel": {"chunk": "k_numeric_chunks", "tile": "k_numeric_tiles"}.get(
+                         os.environ.get("SA_KERNEL", ""), "k_numeric_rowgather"),
                      "frac_of_8TBps_nominal": achieved / 8000.0},
         "gpu_launches": launches,
         "clocks": clk.summary(),
@@ -342,37 +343,39 @@ def main():
 
 
 def run_e2e(cfg, q, me, vols, kernels, rb, re_, m, args, world, dev):
-    """Same metric through the public API with host buffers: every step uploads
-    q/me/vols from pinned host memory, runs symbolic + numeric (+ exact-zero
-    compaction) and reads the CSR back to host memory."""
+    """Same metric through the public API with host buffers: every step calls
+    assemble_block_b200 on a Mesh whose q/me/vols live in pinned host memory:
+    upload, symbolic phase, numeric phase, exact-zero compaction, download of
+    the canonical CSR (int64 indices, f64 values) into pinned host memory."""
     import torch
 
-    from paper_1401_3301_b200 import device as D
-    from paper_1401_3301_b200.assembly import to_host
+    import paper_1401_3301_b200 as P
+    from paper_1401_3301_b200.assembly import assemble_block_b200
 
     pq = torch.from_numpy(q).pin_memory()
     pme = torch.from_numpy(me).pin_memory()
     pv = torch.from_numpy(np.asarray(vols)).pin_memory()
+    mesh = P.Mesh(pq.numpy(), pme.numpy(), pv.numpy())
     h2d = pq.numel() * 8 + pme.numel() * 8 + pv.numel() * 8
     steps = max(2, min(args.steps, 5))
     times = []
     d2h = 0
+    stages = {}
     for i in range(steps + 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        dm = D.DeviceMesh(pq, pme, pv)
-        plan = dm.plan(m, rb, re_)
-        csrs = plan.assemble(kernels)
-        host = []
-        for c in csrs:
-            host.append((c.indptr.cpu().numpy(), c.indices.cpu().numpy(), c.vals.cpu().numpy()))
+        blocks = assemble_block_b200(mesh, kernels, rb, re_, timings=stages if i > 0 else None)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if i > 0:
             times.append(dt)
-        d2h = sum(a.nbytes + b.nbytes + v.nbytes for a, b, v in host)
-        dm.close()
-        del plan, csrs
+        seen, d2h = set(), 0
+        for b in blocks:   # shared pattern arrays cross PCIe once
+            for arr in (b.row_ptr, b.col_idx, b.vals):
+                if id(arr) not in seen:
+                    seen.add(id(arr))
+                    d2h += arr.nbytes
+        del blocks
     t = torch.tensor([statistics.median(times)], dtype=torch.float64, device=dev)
     if world > 1:
         import torch.distributed as dist
@@ -381,7 +384,9 @@ def run_e2e(cfg, q, me, vols, kernels, rb, re_, m, args, world, dev):
     nme = me.shape[1]
     return {"value": nme / float(t.item()), "unit": "elements/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": float(t.item()) * 1e3,
-            "path": "DeviceMesh(host pinned q,me,vols) -> plan (symbolic) -> numeric -> compact -> host CSR",
+            "stages_ms": {k: v / steps for k, v in stages.items()},
+            "path": "assemble_block_b200(Mesh(pinned q, me, vols)): upload -> symbolic -> numeric -> compact -> "
+                    "pinned host CSR (int64 indices)",
             "timing": "host wall clock, median of %d, device synchronized" % len(times)}
 
 

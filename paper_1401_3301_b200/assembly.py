@@ -64,11 +64,45 @@ def _as_descriptor(mesh, kernel):
 def to_host(csr: DeviceCSR, nrows_total: int | None = None) -> SparseMatrix:
     """Download a full-matrix device CSR into the reference's SparseMatrix
     (int64 indices, as sparse.py:53-55)."""
+    import torch
+
     nrows = csr.row_end - csr.row_begin if nrows_total is None else nrows_total
-    row_ptr = csr.indptr.cpu().numpy().astype(np.int64, copy=False)
-    col_idx = csr.indices.cpu().numpy().astype(np.int64)
-    vals = csr.vals.cpu().numpy()
+    # int32 -> int64 on the device (SparseMatrix stores int64, sparse.py:53-55),
+    # then one asynchronous copy per array into pinned host buffers
+    srcs = (csr.indptr, csr.indices.to(torch.int64), csr.vals)
+    outs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in srcs]
+    for o, t in zip(outs, srcs):
+        o.copy_(t, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    row_ptr, col_idx, vals = (o.numpy() for o in outs)
     return SparseMatrix(nrows, csr.ncols, row_ptr, col_idx, vals)
+
+
+def to_host_many(csrs, nrows_total=None) -> list[SparseMatrix]:
+    """Download several results; fused outputs that share one pattern (no
+    exact-zero entries dropped) share the host row_ptr/col_idx arrays, so the
+    pattern crosses PCIe once."""
+    import torch
+
+    cache = {}
+    out = []
+    for c in csrs:
+        key = (c.indptr.data_ptr(), c.indices.data_ptr(), c.indices.numel())
+        if key not in cache:
+            srcs = (c.indptr, c.indices.to(torch.int64))
+            pinned = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in srcs]
+            for o, t in zip(pinned, srcs):
+                o.copy_(t, non_blocking=True)
+            cache[key] = pinned
+        v = torch.empty(c.vals.shape, dtype=c.vals.dtype, pin_memory=True)
+        v.copy_(c.vals, non_blocking=True)
+        out.append((c, cache[key], v))
+    torch.cuda.current_stream().synchronize()
+    res = []
+    for c, (ip, ix), v in out:
+        nrows = c.row_end - c.row_begin if nrows_total is None else nrows_total
+        res.append(SparseMatrix(nrows, c.ncols, ip.numpy(), ix.numpy(), v.numpy()))
+    return res
 
 
 def assemble_device(mesh, kernels, core: str = "SkylakeX", cache: bool = True) -> list[DeviceCSR]:
@@ -82,8 +116,40 @@ def assemble_device(mesh, kernels, core: str = "SkylakeX", cache: bool = True) -
     return dm.plan(m).assemble(kernels)
 
 
-def assemble_many_b200(mesh, kernels, core: str = "SkylakeX") -> list[SparseMatrix]:
-    return [to_host(c) for c in assemble_device(mesh, kernels, core)]
+def assemble_many_b200(mesh, kernels, core: str = "SkylakeX", cache: bool = True) -> list[SparseMatrix]:
+    """Fused drop-in assembly of several kernels on one mesh (e.g. mass +
+    stiffness): one upload, one symbolic phase, one numeric pass."""
+    return to_host_many(assemble_device(mesh, kernels, core, cache))
+
+
+def assemble_block_b200(mesh, kernels, row_begin: int, row_end: int, core: str = "SkylakeX",
+                        timings: dict | None = None):
+    """Rows [row_begin, row_end) of the fused assembly, end to end from host
+    arrays (the per-rank call of the row-block data-parallel path): upload,
+    symbolic, numeric, exact-zero compaction, download.  Returns one
+    (indptr, indices, vals) host block per kernel."""
+    import time
+
+    import torch
+
+    kernels = [_as_descriptor(mesh, k) for k in kernels]
+    t = time.perf_counter()
+    dm = DeviceMesh(mesh.q, mesh.me, getattr(mesh, "vols", None), core=core)
+    torch.cuda.current_stream().synchronize()
+    t1 = time.perf_counter()
+    plan = dm.plan(kernels[0].m, row_begin, row_end)
+    t2 = time.perf_counter()
+    csrs = plan.assemble(kernels)
+    torch.cuda.current_stream().synchronize()
+    t3 = time.perf_counter()
+    out = to_host_many(csrs)
+    t4 = time.perf_counter()
+    dm.close()
+    if timings is not None:
+        for k, v in (("upload_ms", t1 - t), ("symbolic_ms", t2 - t1), ("numeric_ms", t3 - t2),
+                     ("download_ms", t4 - t3), ("free_ms", time.perf_counter() - t4)):
+            timings[k] = timings.get(k, 0.0) + 1e3 * v
+    return out
 
 
 def assemble_b200(mesh, kernel) -> SparseMatrix:

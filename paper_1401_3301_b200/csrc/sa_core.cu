@@ -443,6 +443,16 @@ __global__ void k_tile_verify(const uint32_t *__restrict__ scratch, int stride, 
     if (!__all_sync(0xffffffffu, ok) && lane == 0) atomicOr(bad, 1ull);
 }
 
+// max_i (p[i+1] - p[i]) over a prefix array
+__global__ void k_max_diff(const int64_t *__restrict__ p, int64_t n, unsigned long long *out)
+{
+    unsigned long long m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, (unsigned long long)(p[i + 1] - p[i]));
+    for (int s = 16; s > 0; s >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, s));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
 // dof-level CSR of the block: row m*nl+l has columns m*cols[k]+n
 __global__ void k_dof_csr(const int64_t *__restrict__ colptr, const int32_t *__restrict__ cols, int64_t nnodes,
                           int m, int64_t *__restrict__ indptr, int32_t *__restrict__ indices)
@@ -1317,16 +1327,19 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
         SA_LAUNCH(k_inc_ranks<D>, grid_for(nn, 128), 128, 0, st, (const I *)M->me, P->inc_ptr, P->inc, nn, P->colptr,
                   P->cols);
     }
-    // max node degree (host side from the node-level colptr)
-    std::vector<int64_t> hcp(nn + 1);
-    SA_CUDA_TRY(cudaMemcpyAsync(hcp.data(), P->colptr, (nn + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SA_CUDA_TRY(cudaStreamSynchronize(st));
+    // max node degree: device reduction (no host copy of colptr)
+    SA_CUDA_TRY(cudaMemsetAsync(P->counters + 6, 0, sizeof(int64_t), st));
+    if (nn)
+        SA_LAUNCH(k_max_diff, std::min<int64_t>(grid_for(nn, 256), 148 * 8), 256, 0, st, P->colptr, nn,
+                  (unsigned long long *)(P->counters + 6));
     int64_t md = 0;
-    for (int64_t i = 0; i < nn; ++i) md = std::max(md, hcp[i + 1] - hcp[i]);
+    SA_CUDA_TRY(cudaMemcpyAsync(&md, P->counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SA_CUDA_TRY(cudaStreamSynchronize(st));
     P->max_deg = md;
-    // block numeric kernel data
-    {
-        std::vector<int64_t> hip(nn + 1);
+    // fold programs + templates: only for the tile / chunk kernels
+    if (want_tile_kernel() || want_chunk_kernel()) {
+        std::vector<int64_t> hcp(nn + 1), hip(nn + 1);
+        SA_CUDA_TRY(cudaMemcpyAsync(hcp.data(), P->colptr, (nn + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
         SA_CUDA_TRY(cudaMemcpyAsync(hip.data(), P->inc_ptr, (nn + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
         SA_CUDA_TRY(cudaMallocAsync((void **)&P->inc_e, std::max<int64_t>(P->n_inc, 1) * sizeof(uint32_t), st));
         SA_CUDA_TRY(cudaMallocAsync((void **)&P->fold, std::max<int64_t>((D + 1) * P->n_inc, 1) * sizeof(uint16_t), st));
@@ -1523,6 +1536,28 @@ int SA_CAT(sa_dispatch_d, SA_D)(const sa_plan *P, const NumArgs &a, int ops, int
 #endif
 
 #ifdef SA_ABI
+// Device buffers come from the stream-ordered pool (cudaMallocAsync) whose
+// release threshold is raised once, so repeated mesh/plan construction
+// (re-assembly, e2e) reuses memory instead of re-mapping it.
+static void pool_keep_memory(int device)
+{
+    static bool done[64] = {false};
+    if (device < 0 || device >= 64 || done[device]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[device] = true;
+}
+
+static void free_all(std::initializer_list<void *> ps)
+{
+    cudaDeviceSynchronize();
+    for (void *p : ps)
+        if (p) cudaFreeAsync(p, 0);
+}
+
 // ===========================================================================
 // C ABI
 
@@ -1551,6 +1586,7 @@ int sa_mesh_create(int d, int64_t nq, int64_t nme, const double *q_dev, const in
         return set_error(SA_ERR_CAPACITY, "mesh with nq=%lld nme=%lld exceeds the int32 index range",
                          (long long)nq, (long long)nme);
     SA_TRY(set_device(device));
+    pool_keep_memory(device);
     cudaStream_t st = (cudaStream_t)stream;
     sa_mesh *M = new sa_mesh();
     M->d = d; M->nq = nq; M->nme = nme; M->core = core; M->device = device;
@@ -1558,10 +1594,10 @@ int sa_mesh_create(int d, int64_t nq, int64_t nme, const double *q_dev, const in
     size_t isz = d == 1 ? 8 : 16;
     int rc = SA_OK;
     auto fail = [&](int r) { sa_mesh_destroy(M); return r; };
-    if (cudaMalloc(&M->qv, std::max<int64_t>(nq, 1) * vsz) != cudaSuccess ||
-        cudaMalloc(&M->me, std::max<int64_t>(nme, 1) * isz) != cudaSuccess ||
-        cudaMalloc((void **)&M->vols, std::max<int64_t>(nme, 1) * sizeof(double)) != cudaSuccess ||
-        cudaMalloc((void **)&M->scratch, 8 * sizeof(int64_t)) != cudaSuccess)
+    if (cudaMallocAsync(&M->qv, std::max<int64_t>(nq, 1) * vsz, st) != cudaSuccess ||
+        cudaMallocAsync(&M->me, std::max<int64_t>(nme, 1) * isz, st) != cudaSuccess ||
+        cudaMallocAsync((void **)&M->vols, std::max<int64_t>(nme, 1) * sizeof(double), st) != cudaSuccess ||
+        cudaMallocAsync((void **)&M->scratch, 8 * sizeof(int64_t), st) != cudaSuccess)
         return fail(set_error(SA_ERR_NOMEM, "device allocation for the mesh failed"));
     if (d == 1) rc = sa_mesh_kernels_d1(M, q_dev, me_dev, vols_dev, st);
     else if (d == 2) rc = sa_mesh_kernels_d2(M, q_dev, me_dev, vols_dev, st);
@@ -1582,10 +1618,7 @@ int sa_mesh_vols(const sa_mesh *M, double *vols_dev_out, void *stream)
 int sa_mesh_destroy(sa_mesh *M)
 {
     if (!M) return SA_OK;
-    cudaFree(M->qv);
-    cudaFree(M->me);
-    cudaFree(M->vols);
-    cudaFree(M->scratch);
+    free_all({M->qv, M->me, M->vols, M->scratch});
     delete M;
     return SA_OK;
 }
@@ -1593,13 +1626,9 @@ int sa_mesh_destroy(sa_mesh *M)
 int sa_plan_destroy(sa_plan *P)
 {
     if (!P) return SA_OK;
-    cudaDeviceSynchronize();
-    cudaFree(P->inc_ptr); cudaFree(P->inc); cudaFree(P->colptr); cudaFree(P->cols);
-    cudaFree(P->indptr); cudaFree(P->indices); cudaFree(P->counters); cudaFree(P->scan_tmp);
-    cudaFree(P->inc_e); cudaFree(P->fold);
-    cudaFree(P->tile_e0); cudaFree(P->tile_tm); cudaFree(P->tm_off); cudaFree(P->tm);
-    cudaFree(P->ck_tm); cudaFree(P->ck_pb); cudaFree(P->ck_tm_off); cudaFree(P->ck_tmw); cudaFree(P->ck_flags);
-    cudaFree(P->ck_rs);
+    free_all({P->inc_ptr, P->inc, P->colptr, P->cols, P->indptr, P->indices, P->counters, P->scan_tmp, P->inc_e,
+              P->fold, P->tile_e0, P->tile_tm, P->tm_off, P->tm, P->ck_tm, P->ck_pb, P->ck_tm_off, P->ck_tmw,
+              P->ck_flags, P->ck_rs});
     delete P;
     return SA_OK;
 }
@@ -1620,7 +1649,7 @@ int sa_plan_create(const sa_mesh *M, int m, int64_t row_begin, int64_t row_end, 
     sa_plan *P = new sa_plan();
     P->mesh = M; P->m = m; P->row_begin = row_begin; P->row_end = row_end; P->nrows = row_end - row_begin;
     P->node_begin = row_begin / m; P->node_end = row_end / m; P->nnodes = P->node_end - P->node_begin;
-    if (cudaMalloc((void **)&P->counters, 8 * sizeof(int64_t)) != cudaSuccess) {
+    if (cudaMallocAsync((void **)&P->counters, 8 * sizeof(int64_t), st) != cudaSuccess) {
         delete P;
         return set_error(SA_ERR_NOMEM, "device allocation failed");
     }

@@ -1,0 +1,17 @@
+#!/bin/bash
+# Round evidence: tests, smoke, full bench (C2 + e2e + cpu baseline), per-config
+# numeric benches, launch list and one full ncu capture of the numeric kernel.
+cd "${GRAFT_REPO_ROOT:-$(dirname $0)/..}"
+mkdir -p gpurun_out
+make -s -C oracle
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/ev_pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/ev_pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/ev_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/ev_smoke.log
+timeout 900 python bench.py > gpurun_out/ev_bench_C2.log 2>&1; echo "bench rc=$?" >> gpurun_out/ev_bench_C2.log
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/ev_bench_ref.log 2>&1
+for c in C1 C3 C4; do timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/ev_bench_$c.log 2>&1; done
+CMD="python bench.py --config C2 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
+$CMD > gpurun_out/ev_plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ev_launches_C2.csv $CMD > gpurun_out/ev_ncu1.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k_numeric -s 3 -c 1 -o gpurun_out/ev_prof_C2 -f $CMD > gpurun_out/ev_ncu2.log 2>&1
+echo "ncu rc=$?"
+tail -1 gpurun_out/ev_pytest_gpu.log; tail -1 gpurun_out/ev_smoke.log
