@@ -84,6 +84,8 @@ struct NumArgs {
     const uint2 *inc;
     const int64_t *colptr;
     const int64_t *indptr;
+    const int32_t *cols;  // node-level sorted neighbour nodes (row-gather coordinate cache)
+    int dbg;              // diagnostics (SA_DBG): 1 = loads only, 2 = loads + element math, no folds
     int acc_stride;  // smem accumulator rows per output (m*m*max_deg)
     double *vals[2];
     int64_t *counters;
@@ -548,6 +550,77 @@ __device__ __forceinline__ void element_load2(const NumArgs &a, ElemRaw<D> &r)
     }
 }
 
+// nodal coefficients only (vertex coordinates already in r.x)
+template <int D, int OPS>
+__device__ __forceinline__ void element_load_coeffs(const NumArgs &a, ElemRaw<D> &r)
+{
+#pragma unroll
+    for (int k = 0; k <= D; ++k) {
+        const int vk = r.v[k];
+        if constexpr ((OPS & OP_MASS) != 0) r.W[k] = a.w ? __ldg(a.w + vk) : 0.0;
+        if constexpr ((OPS & OP_ELASTIC) != 0) {
+            r.lam[k] = nodal<D>(a.lamb, a.lamb_const, vk);
+            r.mu[k] = nodal<D>(a.mu, a.mu_const, vk);
+        }
+        if constexpr ((OPS & OP_GENERAL) != 0) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+#pragma unroll
+                for (int j = 0; j < D; ++j)
+                    r.A[k][i][j] = a.A ? __ldg(a.A + (int64_t)vk * D * D + i * D + j) : a.A_const[i * D + j];
+                r.b[k][i] = a.b ? __ldg(a.b + (int64_t)vk * D + i) : 0.0;
+                r.c[k][i] = a.c ? __ldg(a.c + (int64_t)vk * D + i) : 0.0;
+            }
+            r.a0[k] = a.a0 ? __ldg(a.a0 + vk) : a.a0_const;
+        }
+    }
+}
+
+// nodal coefficients only (vertex coordinates already in r.x)
+template <int D, int OPS>
+__device__ __forceinline__ void element_load_coeffs(const NumArgs &a, ElemRaw<D> &r)
+{
+#pragma unroll
+    for (int k = 0; k <= D; ++k) {
+        const int vk = r.v[k];
+        if constexpr ((OPS & OP_MASS) != 0) r.W[k] = a.w ? __ldg(a.w + vk) : 0.0;
+        if constexpr ((OPS & OP_ELASTIC) != 0) {
+            r.lam[k] = nodal<D>(a.lamb, a.lamb_const, vk);
+            r.mu[k] = nodal<D>(a.mu, a.mu_const, vk);
+        }
+        if constexpr ((OPS & OP_GENERAL) != 0) {
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+#pragma unroll
+                for (int j = 0; j < D; ++j)
+                    r.A[k][i][j] = a.A ? __ldg(a.A + (int64_t)vk * D * D + i * D + j) : a.A_const[i * D + j];
+                r.b[k][i] = a.b ? __ldg(a.b + (int64_t)vk * D + i) : 0.0;
+                r.c[k][i] = a.c ? __ldg(a.c + (int64_t)vk * D + i) : 0.0;
+            }
+            r.a0[k] = a.a0 ? __ldg(a.a0 + vk) : a.a0_const;
+        }
+    }
+}
+
+// vertices except the owner's (local vertex alpha, loaded once per row by
+// the caller), then the nodal coefficients
+template <int D, int OPS>
+__device__ __forceinline__ void element_load2_skip(const NumArgs &a, ElemRaw<D> &r, int alpha, const double (&own)[D])
+{
+    if constexpr ((OPS & (OP_STIFF | OP_ELASTIC | OP_GENERAL)) != 0) {
+#pragma unroll
+        for (int k = 0; k <= D; ++k) {
+            if (k == alpha) {
+#pragma unroll
+                for (int c = 0; c < D; ++c) r.x[k][c] = own[c];
+            } else {
+                load_vertex<D>((const typename VecT<D>::type *)a.qv, r.v[k], r.x[k]);
+            }
+        }
+    }
+    element_load_coeffs<D, OPS>(a, r);
+}
+
 // K1: bit-exact gradients and per-element coefficient sums from raw inputs.
 template <int D, int OPS, int CORE>
 __device__ __forceinline__ bool element_compute(const ElemRaw<D> &r, ElemGeo<D> &g)
@@ -671,11 +744,17 @@ __device__ __forceinline__ void krow_runtime(const NumArgs &a, const ElemGeo<D> 
 // accumulators indexed by the 8-bit column ranks stored with each incidence.
 // Used when a node has more than 31 incidences or the block kernel's shared
 // memory does not fit.
-template <int D, int M, int OPS, int CORE>
+template <int D, int M, int OPS, int CORE, int ILP, bool XC>
 __global__ void __launch_bounds__(128) k_numeric_rowgather(NumArgs a)
 {
     constexpr int NOUT = n_outputs<OPS>();
     extern __shared__ double smem_acc[];
+    // XC: the row's neighbour coordinates (and node ids) are cached in the
+    // owner's private shared memory, so an incidence gathers only its record
+    // and volume -- the element's vertices are read from the cache by rank.
+    const int maxdeg = a.acc_stride / (M * M);
+    double *xc = smem_acc + (size_t)NOUT * a.acc_stride * blockDim.x;                 // [maxdeg*D][nthr]
+    int *nidc = reinterpret_cast<int *>(xc + (size_t)maxdeg * D * blockDim.x);        // [maxdeg][nthr]
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int64_t nl = blockIdx.x * (int64_t)blockDim.x + tid;
     int nz[NOUT];
@@ -690,15 +769,50 @@ __global__ void __launch_bounds__(128) k_numeric_rowgather(NumArgs a)
             for (int l = 0; l < M; ++l)
                 for (int k = 0; k < deg_stride; ++k)
                     smem_acc[(o * a.acc_stride + l * row_stride + k) * nthr + tid] = 0.0;
+        if constexpr (XC) {
+            for (int k = 0; k < deg; ++k) {
+                const int node = __ldg(a.cols + c0 + k);
+                double x[D];
+                load_vertex<D>((const typename VecT<D>::type *)a.qv, node, x);
+                nidc[k * nthr + tid] = node;
+#pragma unroll
+                for (int c = 0; c < D; ++c) xc[(k * D + c) * nthr + tid] = x[c];
+            }
+        }
+        auto cached_load = [&](uint2 rec, ElemRaw<D> &r) {
+            r.vol = __ldg(a.vols + (rec.x & 0x3fffffffu));
+#pragma unroll
+            for (int b = 0; b <= D; ++b) {
+                const int rk = (rec.y >> (8 * b)) & 0xff;
+                r.v[b] = nidc[rk * nthr + tid];
+#pragma unroll
+                for (int c = 0; c < D; ++c) r.x[b][c] = xc[(rk * D + c) * nthr + tid];
+            }
+            element_load_coeffs<D, OPS>(a, r);
+        };
         const int64_t t1 = a.inc_ptr[nl + 1];
         int64_t emin = INT64_MAX;
         constexpr int MM = M * M;
+        double dsum = 0.0;
         auto fold = [&](const ElemRaw<D> &x, uint2 rec) {
+            if (a.dbg == 1) {   // diagnostics: memory traffic only
+#pragma unroll
+                for (int b = 0; b <= D; ++b)
+#pragma unroll
+                    for (int c = 0; c < D; ++c) dsum += x.x[b][c];
+                dsum += x.vol + (double)x.v[0] + (double)rec.y;
+                return;
+            }
             ElemGeo<D> g;
             const int64_t e = rec.x & 0x3fffffffu;
             if (element_compute<D, OPS, CORE>(x, g)) emin = min(emin, e);
             double vals[(D + 1) * NOUT * MM];
             krow_runtime<D, M, OPS>(a, g, rec.x >> 30, vals);
+            if (a.dbg == 2) {   // diagnostics: no folds
+#pragma unroll
+                for (int i = 0; i < (D + 1) * NOUT * MM; ++i) dsum += vals[i];
+                return;
+            }
 #pragma unroll
             for (int b = 0; b <= D; ++b) {
                 const int r = (rec.y >> (8 * b)) & 0xff;
@@ -713,32 +827,71 @@ __global__ void __launch_bounds__(128) k_numeric_rowgather(NumArgs a)
             }
         };
         int64_t t = a.inc_ptr[nl];
-        for (; t + 1 < t1; t += 2) {
+        for (; ILP == 2 && t + 1 < t1; t += 2) {
             const uint2 r1 = __ldg(a.inc + t), r2 = __ldg(a.inc + t + 1);
             ElemRaw<D> x1, x2;
-            element_load1<D, OPS>(a, r1.x & 0x3fffffffu, x1);
-            element_load1<D, OPS>(a, r2.x & 0x3fffffffu, x2);
-            element_load2<D, OPS>(a, x1);
-            element_load2<D, OPS>(a, x2);
+            if constexpr (XC) {
+                cached_load(r1, x1);
+                cached_load(r2, x2);
+            } else {
+                element_load1<D, OPS>(a, r1.x & 0x3fffffffu, x1);
+                element_load1<D, OPS>(a, r2.x & 0x3fffffffu, x2);
+                element_load2<D, OPS>(a, x1);
+                element_load2<D, OPS>(a, x2);
+            }
             fold(x1, r1);
             fold(x2, r2);
         }
-        if (t < t1) {
+        for (; t < t1; ++t) {
             const uint2 r1 = __ldg(a.inc + t);
             ElemRaw<D> x1;
-            element_load1<D, OPS>(a, r1.x & 0x3fffffffu, x1);
-            element_load2<D, OPS>(a, x1);
+            if constexpr (XC) {
+                cached_load(r1, x1);
+            } else {
+                element_load1<D, OPS>(a, r1.x & 0x3fffffffu, x1);
+                element_load2<D, OPS>(a, x1);
+            }
             fold(x1, r1);
         }
         if (emin != INT64_MAX) atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)emin);
-        for (int o = 0; o < NOUT; ++o) {
-            double *out = a.vals[o];
-            for (int l = 0; l < M; ++l) {
-                const int64_t p = a.indptr[M * nl + l];
-                for (int k = 0; k < deg_stride; ++k) {
-                    double val = smem_acc[(o * a.acc_stride + l * row_stride + k) * nthr + tid];
-                    out[p + k] = val;
+        if (a.dbg) smem_acc[tid] = dsum;
+    }
+    // Stores.  When the warp's 32 rows all have the same degree (every warp
+    // inside a structured mesh), their CSR segments form one contiguous run
+    // and the warp writes it coalesced from the owners' accumulators;
+    // otherwise each owner writes its own row segment.
+    __syncwarp();
+    {
+        const unsigned full = 0xffffffffu;
+        const int lane = tid & 31, wbase = tid & ~31;
+        const bool active = nl < a.nnodes;
+        const int mydeg = active ? (int)(a.colptr[nl + 1] - a.colptr[nl]) : -1;
+        const int d0 = __shfl_sync(full, mydeg, 0);
+        const bool uniform = __all_sync(full, mydeg == d0) && d0 > 0;
+        const int row_stride = a.acc_stride / M;
+        if (uniform) {
+            const int64_t base = __shfl_sync(full, active ? a.indptr[M * nl] : (int64_t)0, 0);
+            const int run = M * M * d0, mdeg = M * d0;
+            for (int i = lane; i < 32 * run; i += 32) {
+                const int r = i / run, j = i - r * run;
+                const int l = j / mdeg, k = j - l * mdeg;
+#pragma unroll
+                for (int o = 0; o < NOUT; ++o) {
+                    const double val = smem_acc[(o * a.acc_stride + l * row_stride + k) * nthr + wbase + r];
+                    a.vals[o][base + i] = val;
                     nz[o] += (val == 0.0);
+                }
+            }
+        } else if (active) {
+            for (int o = 0; o < NOUT; ++o) {
+                double *out = a.vals[o];
+                for (int l = 0; l < M; ++l) {
+                    const int64_t p = a.indptr[M * nl + l];
+                    for (int k = 0; k < M * mydeg; ++k) {
+                        const double val = smem_acc[(o * a.acc_stride + l * row_stride + k) * nthr + tid];
+                        out[p + k] = val;
+                        nz[o] += (val == 0.0);
+                    }
                 }
             }
         }
@@ -1385,18 +1538,28 @@ template <int D, int M, int OPS, int CORE>
 int launch_rowgather(const NumArgs &a, int64_t nnodes, cudaStream_t st)
 {
     constexpr int NOUT = n_outputs<OPS>();
+    // SA_ILP (1|2): incidences in flight per thread (default 1 in 2D, 2 in 3D);
+    // SA_XCACHE (0|1): neighbour-coordinate cache (default off: slower, measured)
+    const char *ilp_s = getenv("SA_ILP"), *xc_s = getenv("SA_XCACHE");
+    const int ilp = ilp_s ? atoi(ilp_s) : (D == 3 ? 2 : 1);
+    const bool xc = xc_s ? atoi(xc_s) != 0 : false;
+    const int maxdeg = a.acc_stride / (M * M);
+    const size_t per_thread = (size_t)NOUT * a.acc_stride * sizeof(double) +
+                              (xc ? (size_t)maxdeg * (D * sizeof(double) + sizeof(int)) : 0);
     int block = 128;
-    size_t smem = (size_t)NOUT * a.acc_stride * block * sizeof(double);
-    while (smem > 200 * 1024 && block > 32) { block /= 2; smem /= 2; }
+    while (per_thread * block > 100 * 1024 && block > 32) block /= 2;
+    const size_t smem = per_thread * block;
     if (smem > 200 * 1024)
-        return set_error(SA_ERR_CAPACITY, "row accumulators need %zu B of shared memory per 32 threads", smem);
-    auto kern = k_numeric_rowgather<D, M, OPS, CORE>;
+        return set_error(SA_ERR_CAPACITY, "row accumulators need %zu B of shared memory per %d threads", smem, block);
+    void (*kern)(NumArgs);
+    if (xc) kern = ilp == 2 ? k_numeric_rowgather<D, M, OPS, CORE, 2, true> : k_numeric_rowgather<D, M, OPS, CORE, 1, true>;
+    else kern = ilp == 2 ? k_numeric_rowgather<D, M, OPS, CORE, 2, false> : k_numeric_rowgather<D, M, OPS, CORE, 1, false>;
     SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (nnodes) SA_LAUNCH(kern, grid_for(nnodes, block), block, smem, st, a);
     return SA_OK;
 }
 
-// returns SA_OK after launching, 1000 when the tile kernel does not fit
+// returns SA_OK after launching, 1000 when the kernel's staging does not fit
 #define SA_TRY_OR_FALL(...)                  \
     do {                                     \
         int _r = (__VA_ARGS__);              \
@@ -1711,7 +1874,8 @@ int sa_numeric(sa_plan *P, int ops, const sa_coeffs *cf, double *const *vals_dev
     memset(&a, 0, sizeof a);
     a.qv = M->qv; a.me = M->me; a.vols = M->vols;
     a.nnodes = P->nnodes; a.node_begin = P->node_begin;
-    a.inc_ptr = P->inc_ptr; a.inc = P->inc; a.colptr = P->colptr; a.indptr = P->indptr;
+    a.inc_ptr = P->inc_ptr; a.inc = P->inc; a.colptr = P->colptr; a.indptr = P->indptr; a.cols = P->cols;
+    a.dbg = getenv("SA_DBG") ? atoi(getenv("SA_DBG")) : 0;
     a.acc_stride = (int)(P->m * P->m * std::max<int64_t>(P->max_deg, 1));
     int nout = 0;
     for (int bit = 1; bit <= 8; bit <<= 1)
