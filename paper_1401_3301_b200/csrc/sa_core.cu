@@ -576,51 +576,6 @@ __device__ __forceinline__ void element_load_coeffs(const NumArgs &a, ElemRaw<D>
     }
 }
 
-// nodal coefficients only (vertex coordinates already in r.x)
-template <int D, int OPS>
-__device__ __forceinline__ void element_load_coeffs(const NumArgs &a, ElemRaw<D> &r)
-{
-#pragma unroll
-    for (int k = 0; k <= D; ++k) {
-        const int vk = r.v[k];
-        if constexpr ((OPS & OP_MASS) != 0) r.W[k] = a.w ? __ldg(a.w + vk) : 0.0;
-        if constexpr ((OPS & OP_ELASTIC) != 0) {
-            r.lam[k] = nodal<D>(a.lamb, a.lamb_const, vk);
-            r.mu[k] = nodal<D>(a.mu, a.mu_const, vk);
-        }
-        if constexpr ((OPS & OP_GENERAL) != 0) {
-#pragma unroll
-            for (int i = 0; i < D; ++i) {
-#pragma unroll
-                for (int j = 0; j < D; ++j)
-                    r.A[k][i][j] = a.A ? __ldg(a.A + (int64_t)vk * D * D + i * D + j) : a.A_const[i * D + j];
-                r.b[k][i] = a.b ? __ldg(a.b + (int64_t)vk * D + i) : 0.0;
-                r.c[k][i] = a.c ? __ldg(a.c + (int64_t)vk * D + i) : 0.0;
-            }
-            r.a0[k] = a.a0 ? __ldg(a.a0 + vk) : a.a0_const;
-        }
-    }
-}
-
-// vertices except the owner's (local vertex alpha, loaded once per row by
-// the caller), then the nodal coefficients
-template <int D, int OPS>
-__device__ __forceinline__ void element_load2_skip(const NumArgs &a, ElemRaw<D> &r, int alpha, const double (&own)[D])
-{
-    if constexpr ((OPS & (OP_STIFF | OP_ELASTIC | OP_GENERAL)) != 0) {
-#pragma unroll
-        for (int k = 0; k <= D; ++k) {
-            if (k == alpha) {
-#pragma unroll
-                for (int c = 0; c < D; ++c) r.x[k][c] = own[c];
-            } else {
-                load_vertex<D>((const typename VecT<D>::type *)a.qv, r.v[k], r.x[k]);
-            }
-        }
-    }
-    element_load_coeffs<D, OPS>(a, r);
-}
-
 // K1: bit-exact gradients and per-element coefficient sums from raw inputs.
 template <int D, int OPS, int CORE>
 __device__ __forceinline__ bool element_compute(const ElemRaw<D> &r, ElemGeo<D> &g)
