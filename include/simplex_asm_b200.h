@@ -104,6 +104,10 @@ typedef struct sa_coeffs {
     const double *a0;    /* general: (nq,);  NULL = a0_const               */
     double A_const[9];
     double a0_const;
+    /* general, preferred: nodal AoS, 16 doubles per node
+     * [A (3x3 row-major, zero-padded for d < 3) | b (3) | c (3) | a0], one
+     * 128-byte line per node; overrides A/b/c/a0 when non-NULL */
+    const double *gen_packed;
 } sa_coeffs;
 
 /* Assemble the values of every structural entry of the block into

@@ -37,6 +37,7 @@ class SaCoeffs(ctypes.Structure):
         ("mu", ctypes.c_void_p), ("mu_const", ctypes.c_double),
         ("A", ctypes.c_void_p), ("b", ctypes.c_void_p), ("c", ctypes.c_void_p), ("a0", ctypes.c_void_p),
         ("A_const", ctypes.c_double * 9), ("a0_const", ctypes.c_double),
+        ("gen_packed", ctypes.c_void_p),
     ]
 
 

@@ -95,6 +95,7 @@ struct NumArgs {
     const double *mu; double mu_const;
     const double *A; const double *b; const double *c; const double *a0;
     double A_const[9]; double a0_const;
+    const double *gen_packed;  // (nq, 16) AoS [A(9) b(3) c(3) a0] or NULL
     double mass_coef_diag, mass_coef_off;  // 2/((d+1)(d+2)(d+3)), 1/(...) as Python computes them
     double mass_wc;  // constant weight: (wsum + w) + w, the same for every (alpha, beta)
 };
@@ -511,7 +512,10 @@ struct ElemRaw {
     double vol;
     double x[D + 1][D];
     double W[D + 1], lam[D + 1], mu[D + 1];
-    double A[D + 1][D][D], b[D + 1][D], c[D + 1][D], a0[D + 1];
+    // general: coefficient sums accumulated while loading (in vertex order,
+    // as the reference-order restatement sums them) + the per-vertex terms
+    double As[D][D], bs[D], cs[D], a0s;
+    double bv[D + 1][D], cv[D + 1][D], a0v[D + 1];
 };
 
 template <int D, int OPS>
@@ -537,15 +541,42 @@ __device__ __forceinline__ void element_load2(const NumArgs &a, ElemRaw<D> &r)
             r.mu[k] = nodal<D>(a.mu, a.mu_const, vk);
         }
         if constexpr ((OPS & OP_GENERAL) != 0) {
+            if (a.gen_packed) {
+                // one 128-byte line per node: [A 3x3 | b | c | a0]
+                const double *pp = a.gen_packed + (int64_t)vk * 16;
+                double w[16];
 #pragma unroll
-            for (int i = 0; i < D; ++i) {
+                for (int h = 0; h < 4; ++h) ldg256(pp + 4 * h, w[4 * h], w[4 * h + 1], w[4 * h + 2], w[4 * h + 3]);
 #pragma unroll
-                for (int j = 0; j < D; ++j)
-                    r.A[k][i][j] = a.A ? __ldg(a.A + (int64_t)vk * D * D + i * D + j) : a.A_const[i * D + j];
-                r.b[k][i] = a.b ? __ldg(a.b + (int64_t)vk * D + i) : 0.0;
-                r.c[k][i] = a.c ? __ldg(a.c + (int64_t)vk * D + i) : 0.0;
+                for (int i = 0; i < D; ++i) {
+#pragma unroll
+                    for (int j = 0; j < D; ++j) r.As[i][j] = k == 0 ? w[i * 3 + j] : SA_ADD(r.As[i][j], w[i * 3 + j]);
+                    r.bv[k][i] = w[9 + i];
+                    r.cv[k][i] = w[12 + i];
+                    r.bs[i] = k == 0 ? w[9 + i] : SA_ADD(r.bs[i], w[9 + i]);
+                    r.cs[i] = k == 0 ? w[12 + i] : SA_ADD(r.cs[i], w[12 + i]);
+                }
+                r.a0v[k] = w[15];
+                r.a0s = k == 0 ? w[15] : SA_ADD(r.a0s, w[15]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+#pragma unroll
+                    for (int j = 0; j < D; ++j) {
+                        const double t = a.A ? __ldg(a.A + (int64_t)vk * D * D + i * D + j) : a.A_const[i * D + j];
+                        r.As[i][j] = k == 0 ? t : SA_ADD(r.As[i][j], t);
+                    }
+                    const double tb = a.b ? __ldg(a.b + (int64_t)vk * D + i) : 0.0;
+                    const double tc = a.c ? __ldg(a.c + (int64_t)vk * D + i) : 0.0;
+                    r.bv[k][i] = tb;
+                    r.cv[k][i] = tc;
+                    r.bs[i] = k == 0 ? tb : SA_ADD(r.bs[i], tb);
+                    r.cs[i] = k == 0 ? tc : SA_ADD(r.cs[i], tc);
+                }
+                const double t0 = a.a0 ? __ldg(a.a0 + vk) : a.a0_const;
+                r.a0v[k] = t0;
+                r.a0s = k == 0 ? t0 : SA_ADD(r.a0s, t0);
             }
-            r.a0[k] = a.a0 ? __ldg(a.a0 + vk) : a.a0_const;
         }
     }
 }
@@ -563,15 +594,42 @@ __device__ __forceinline__ void element_load_coeffs(const NumArgs &a, ElemRaw<D>
             r.mu[k] = nodal<D>(a.mu, a.mu_const, vk);
         }
         if constexpr ((OPS & OP_GENERAL) != 0) {
+            if (a.gen_packed) {
+                // one 128-byte line per node: [A 3x3 | b | c | a0]
+                const double *pp = a.gen_packed + (int64_t)vk * 16;
+                double w[16];
 #pragma unroll
-            for (int i = 0; i < D; ++i) {
+                for (int h = 0; h < 4; ++h) ldg256(pp + 4 * h, w[4 * h], w[4 * h + 1], w[4 * h + 2], w[4 * h + 3]);
 #pragma unroll
-                for (int j = 0; j < D; ++j)
-                    r.A[k][i][j] = a.A ? __ldg(a.A + (int64_t)vk * D * D + i * D + j) : a.A_const[i * D + j];
-                r.b[k][i] = a.b ? __ldg(a.b + (int64_t)vk * D + i) : 0.0;
-                r.c[k][i] = a.c ? __ldg(a.c + (int64_t)vk * D + i) : 0.0;
+                for (int i = 0; i < D; ++i) {
+#pragma unroll
+                    for (int j = 0; j < D; ++j) r.As[i][j] = k == 0 ? w[i * 3 + j] : SA_ADD(r.As[i][j], w[i * 3 + j]);
+                    r.bv[k][i] = w[9 + i];
+                    r.cv[k][i] = w[12 + i];
+                    r.bs[i] = k == 0 ? w[9 + i] : SA_ADD(r.bs[i], w[9 + i]);
+                    r.cs[i] = k == 0 ? w[12 + i] : SA_ADD(r.cs[i], w[12 + i]);
+                }
+                r.a0v[k] = w[15];
+                r.a0s = k == 0 ? w[15] : SA_ADD(r.a0s, w[15]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < D; ++i) {
+#pragma unroll
+                    for (int j = 0; j < D; ++j) {
+                        const double t = a.A ? __ldg(a.A + (int64_t)vk * D * D + i * D + j) : a.A_const[i * D + j];
+                        r.As[i][j] = k == 0 ? t : SA_ADD(r.As[i][j], t);
+                    }
+                    const double tb = a.b ? __ldg(a.b + (int64_t)vk * D + i) : 0.0;
+                    const double tc = a.c ? __ldg(a.c + (int64_t)vk * D + i) : 0.0;
+                    r.bv[k][i] = tb;
+                    r.cv[k][i] = tc;
+                    r.bs[i] = k == 0 ? tb : SA_ADD(r.bs[i], tb);
+                    r.cs[i] = k == 0 ? tc : SA_ADD(r.cs[i], tc);
+                }
+                const double t0 = a.a0 ? __ldg(a.a0 + vk) : a.a0_const;
+                r.a0v[k] = t0;
+                r.a0s = k == 0 ? t0 : SA_ADD(r.a0s, t0);
             }
-            r.a0[k] = a.a0 ? __ldg(a.a0 + vk) : a.a0_const;
         }
     }
 }
@@ -601,18 +659,18 @@ __device__ __forceinline__ bool element_compute(const ElemRaw<D> &r, ElemGeo<D> 
     }
     if constexpr ((OPS & OP_GENERAL) != 0) {
 #pragma unroll
+        for (int i = 0; i < D; ++i) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) g.As[i][j] = r.As[i][j];
+            g.bs[i] = r.bs[i];
+            g.cs[i] = r.cs[i];
+        }
+        g.a0s = r.a0s;
+#pragma unroll
         for (int k = 0; k <= D; ++k) {
 #pragma unroll
-            for (int i = 0; i < D; ++i) {
-#pragma unroll
-                for (int j = 0; j < D; ++j) g.As[i][j] = k == 0 ? r.A[0][i][j] : SA_ADD(g.As[i][j], r.A[k][i][j]);
-                g.bv[k][i] = r.b[k][i];
-                g.cv[k][i] = r.c[k][i];
-                g.bs[i] = k == 0 ? r.b[0][i] : SA_ADD(g.bs[i], r.b[k][i]);
-                g.cs[i] = k == 0 ? r.c[0][i] : SA_ADD(g.cs[i], r.c[k][i]);
-            }
-            g.a0v[k] = r.a0[k];
-            g.a0s = k == 0 ? r.a0[0] : SA_ADD(g.a0s, r.a0[k]);
+            for (int i = 0; i < D; ++i) { g.bv[k][i] = r.bv[k][i]; g.cv[k][i] = r.cv[k][i]; }
+            g.a0v[k] = r.a0v[k];
         }
     }
     return degenerate;
@@ -1496,7 +1554,7 @@ int launch_rowgather(const NumArgs &a, int64_t nnodes, cudaStream_t st)
     // SA_ILP (1|2): incidences in flight per thread (default 1 in 2D, 2 in 3D);
     // SA_XCACHE (0|1): neighbour-coordinate cache (default off: slower, measured)
     const char *ilp_s = getenv("SA_ILP"), *xc_s = getenv("SA_XCACHE");
-    const int ilp = ilp_s ? atoi(ilp_s) : (D == 3 ? 2 : 1);
+    const int ilp = ilp_s ? atoi(ilp_s) : ((D == 3 && !(OPS & OP_GENERAL)) ? 2 : 1);
     const bool xc = xc_s ? atoi(xc_s) != 0 : false;
     const int maxdeg = a.acc_stride / (M * M);
     const size_t per_thread = (size_t)NOUT * a.acc_stride * sizeof(double) +
@@ -1842,7 +1900,7 @@ int sa_numeric(sa_plan *P, int ops, const sa_coeffs *cf, double *const *vals_dev
     a.w = cf->w; a.w_const = cf->w_const;
     a.lamb = cf->lamb; a.lamb_const = cf->lamb_const;
     a.mu = cf->mu; a.mu_const = cf->mu_const;
-    a.A = cf->A; a.b = cf->b; a.c = cf->c; a.a0 = cf->a0;
+    a.A = cf->A; a.b = cf->b; a.c = cf->c; a.a0 = cf->a0; a.gen_packed = cf->gen_packed;
     memcpy(a.A_const, cf->A_const, sizeof a.A_const);
     a.a0_const = cf->a0_const;
     const double den = (double)((d + 1) * (d + 2) * (d + 3));

@@ -35,15 +35,21 @@ template <> struct IdxT<1> { typedef int2 type; };
 template <> struct IdxT<2> { typedef int4 type; };
 template <> struct IdxT<3> { typedef int4 type; };
 
+// One 32-byte read-only load (sm_100: LDG.E.ENL2.256): a whole sector per
+// lane in a single request, half the L1 requests of two 16-byte loads.
+__device__ __forceinline__ void ldg256(const void *p, double &a, double &b, double &c, double &d)
+{
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+
 template <int D>
 __device__ __forceinline__ void load_vertex(const typename VecT<D>::type *__restrict__ qv, int v, double (&x)[D])
 {
     if constexpr (D == 1) { x[0] = __ldg(qv + v); }
     else if constexpr (D == 2) { double2 t = __ldg(qv + v); x[0] = t.x; x[1] = t.y; }
     else {
-        const double2 *p = reinterpret_cast<const double2 *>(qv + v);
-        double2 t0 = __ldg(p), t1 = __ldg(p + 1);
-        x[0] = t0.x; x[1] = t0.y; x[2] = t1.x;
+        double pad;
+        ldg256(qv + v, x[0], x[1], x[2], pad);
     }
 }
 

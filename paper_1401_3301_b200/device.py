@@ -189,6 +189,8 @@ class Plan:
                     c.mu = up(k.mu)
                 else:
                     c.mu_const = k.mu_const
+            elif k.op == "general" and hasattr(k, "packed"):
+                c.gen_packed = up(k.packed().reshape(-1))
             elif k.op == "general":
                 d = self.dmesh.d
                 if k.A is not None:
@@ -207,10 +209,18 @@ class Plan:
                 del d
         return c, keep
 
-    def numeric(self, kernels, out=None, stream=None, sync: bool = True):
+    def resident_coeffs(self, kernels):
+        """Upload the kernels' nodal coefficients once and keep them in HBM;
+        pass the result as ``numeric(..., coeffs=...)`` to re-assemble without
+        re-uploading (the coefficient arrays must not change meanwhile)."""
+        order = sorted(kernels, key=lambda k: OP_BITS[k.op])
+        return self.coeffs(order)
+
+    def numeric(self, kernels, out=None, stream=None, sync: bool = True, coeffs=None):
         """Values of every structural entry for each kernel (ascending op-bit
         order).  Returns (list of vals tensors, list of exact-zero counts or
-        None when sync=False)."""
+        None when sync=False).  ``coeffs`` = ``resident_coeffs(kernels)`` skips
+        the host->device upload of the nodal coefficients."""
         ops = 0
         for k in kernels:
             ops |= OP_BITS[k.op]
@@ -219,7 +229,7 @@ class Plan:
         dev = self.dmesh.device
         if out is None:
             out = [torch.empty(max(self.nnz, 1), dtype=torch.float64, device=dev) for _ in range(n)]
-        cf, keep = self.coeffs(order)
+        cf, keep = self.coeffs(order) if coeffs is None else coeffs
         ptrs = (ctypes.c_void_p * 4)(*[o.data_ptr() for o in out] + [0] * (4 - n))
         nz = (ctypes.c_int64 * 4)()
         with torch.cuda.device(dev):

@@ -127,3 +127,23 @@ class GeneralKernel:
         else:
             self.a0, self.a0_const = nodal_values(a0, q)
         self.symmetric = False
+        self._packed = None
+
+    def packed(self) -> np.ndarray:
+        """Nodal coefficients as one 128-byte record per node,
+        [A (3x3, zero-padded) | b (3) | c (3) | a0] -- the device layout
+        (one cache line per vertex gather instead of 16 scattered loads)."""
+        if self._packed is None:
+            q = self.mesh.q
+            d, nq = q.shape
+            p = np.zeros((nq, 16))
+            A = self.A if self.A is not None else np.broadcast_to(self.A_const, (nq, d, d))
+            for i in range(d):
+                p[:, 3 * i:3 * i + d] = A[:, i, :]
+            if self.b is not None:
+                p[:, 9:9 + d] = self.b
+            if self.c is not None:
+                p[:, 12:12 + d] = self.c
+            p[:, 15] = self.a0 if self.a0 is not None else self.a0_const
+            self._packed = p
+        return self._packed
