@@ -54,7 +54,22 @@ def make_mesh(cfg, vols_on_device=True):
 
     q, me = P.hypercube_arrays(cfg["d"], cfg["n"])
     q = P.jitter_interior(q, cfg["n"], 0.2 if cfg["d"] == 2 else 0.15, cfg["seed"])
+    if os.environ.get("SA_BENCH_RENUMBER") == "morton":   # locality experiment
+        q, me = _morton_renumber(q, me, cfg["n"])
     return q, me
+
+
+def _morton_renumber(q, me, n):
+    d = q.shape[0]
+    g = np.rint(q * n).astype(np.int64)
+    key = np.zeros(q.shape[1], dtype=np.int64)
+    for bit in range(12):
+        for a in range(d):
+            key |= ((g[a] >> bit) & 1) << (bit * d + (d - 1 - a))
+    perm = np.argsort(key, kind="stable")        # new -> old
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(perm.size)
+    return np.ascontiguousarray(q[:, perm]), np.ascontiguousarray(inv[me])
 
 
 def make_kernels(cfg, mesh):

@@ -54,6 +54,9 @@ def load(build_if_missing: bool = True):
     if _lib is not None:
         return _lib
     path = _build.LIB_PATH
+    override = os.environ.get("SA_LIB_PATH")   # A/B experiments: a prebuilt variant
+    if override:
+        path, build_if_missing = override, False
     if build_if_missing:
         try:
             _build.build()

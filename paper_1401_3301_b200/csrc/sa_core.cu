@@ -34,6 +34,19 @@ struct sa_mesh {
     int64_t *scratch = nullptr;  // [0] bad index
 };
 
+// Warp-interleaved incidence record (row-gather kernel): everything an
+// incidence needs besides the vertex coordinates / nodal coefficients, in one
+// 32-byte sector.  Records of the 32 rows of a warp are interleaved
+// (record k of lane j at wseg[w] + 32 k + j), so each step of the warp reads
+// one contiguous 1 KB run instead of three dependent gathers (record,
+// connectivity, volume).
+struct __align__(32) IncRec {
+    uint32_t ea;      // e | alpha << 30
+    uint32_t ranks;   // 4 x 8-bit column ranks of the element's vertices in the row
+    int32_t v[4];     // the element's vertices (unused slots 0)
+    double vol;       // mesh.vols[e]
+};
+
 struct sa_plan {
     const sa_mesh *mesh = nullptr;
     int m = 1;
@@ -48,6 +61,9 @@ struct sa_plan {
     int32_t *indices = nullptr;   // (nnz) global column dofs
     int64_t *counters = nullptr;  // [0..3] zero counts per output, [4] bad element, [5] capacity flag
     int64_t *scan_tmp = nullptr;
+    IncRec *winc = nullptr;       // warp-interleaved records (padded to each warp's max degree)
+    int64_t *wseg = nullptr;      // (nwarps+1) record offset of each warp of 32 node rows
+    int64_t n_winc = 0;
     // block numeric kernel: compact incidences + fold program
     uint32_t *inc_e = nullptr;    // (n_inc) e | alpha<<30
     uint16_t *fold = nullptr;     // ((d+1) n_inc) per slot: u | beta<<6 | last<<8
@@ -82,10 +98,12 @@ struct NumArgs {
     int64_t node_begin;
     const int64_t *inc_ptr;
     const uint2 *inc;
+    const IncRec *winc;   // warp-interleaved records (row-gather), or NULL
+    const int64_t *wseg;
     const int64_t *colptr;
     const int64_t *indptr;
     const int32_t *cols;  // node-level sorted neighbour nodes (row-gather coordinate cache)
-    int dbg;              // diagnostics (SA_DBG): 1 = loads only, 2 = loads + element math, no folds
+    int dbg;              // diagnostics (SA_DBG): 1 = loads only, 2 = loads + element math, no folds, 3 = stores only
     int acc_stride;  // smem accumulator rows per output (m*m*max_deg)
     double *vals[2];
     int64_t *counters;
@@ -269,6 +287,42 @@ __global__ void k_inc_ranks(const typename IdxT<D>::type *__restrict__ me, const
         }
         rec.y = ranks;
         inc[t] = rec;
+    }
+}
+
+// records per warp of 32 node rows: 32 x the warp's largest incidence count
+__global__ void k_warp_span(const int64_t *__restrict__ inc_ptr, int64_t nnodes, int64_t *__restrict__ span)
+{
+    const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t r0 = w * 32;
+    if (r0 >= nnodes) return;
+    const int64_t r1 = min(r0 + 32, nnodes);
+    int64_t md = 0;
+    for (int64_t r = r0; r < r1; ++r) md = max(md, inc_ptr[r + 1] - inc_ptr[r]);
+    span[w] = 32 * md;
+}
+
+template <int D>
+__global__ void k_winc_fill(const typename IdxT<D>::type *__restrict__ me, const double *__restrict__ vols,
+                            const int64_t *__restrict__ inc_ptr, const uint2 *__restrict__ inc, int64_t nnodes,
+                            const int64_t *__restrict__ wseg, IncRec *__restrict__ winc)
+{
+    const int64_t nl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (nl >= nnodes) return;
+    IncRec *out = winc + wseg[nl >> 5] + (nl & 31);
+    const int64_t t0 = inc_ptr[nl], n = inc_ptr[nl + 1] - t0;
+    for (int64_t k = 0; k < n; ++k) {
+        const uint2 rec = inc[t0 + k];
+        const int64_t e = rec.x & 0x3fffffffu;
+        int v[D + 1];
+        load_element<D>(me, e, v);
+        IncRec r;
+        r.ea = rec.x;
+        r.ranks = rec.y;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) r.v[a] = a <= D ? v[a < D + 1 ? a : 0] : 0;
+        r.vol = vols[e];
+        out[32 * k] = r;
     }
 }
 
@@ -525,63 +579,7 @@ __device__ __forceinline__ void element_load1(const NumArgs &a, int64_t e, ElemR
     r.vol = __ldg(a.vols + e);
 }
 
-template <int D, int OPS>
-__device__ __forceinline__ void element_load2(const NumArgs &a, ElemRaw<D> &r)
-{
-    if constexpr ((OPS & (OP_STIFF | OP_ELASTIC | OP_GENERAL)) != 0) {
-#pragma unroll
-        for (int k = 0; k <= D; ++k) load_vertex<D>((const typename VecT<D>::type *)a.qv, r.v[k], r.x[k]);
-    }
-#pragma unroll
-    for (int k = 0; k <= D; ++k) {
-        const int vk = r.v[k];
-        if constexpr ((OPS & OP_MASS) != 0) r.W[k] = a.w ? __ldg(a.w + vk) : 0.0;
-        if constexpr ((OPS & OP_ELASTIC) != 0) {
-            r.lam[k] = nodal<D>(a.lamb, a.lamb_const, vk);
-            r.mu[k] = nodal<D>(a.mu, a.mu_const, vk);
-        }
-        if constexpr ((OPS & OP_GENERAL) != 0) {
-            if (a.gen_packed) {
-                // one 128-byte line per node: [A 3x3 | b | c | a0]
-                const double *pp = a.gen_packed + (int64_t)vk * 16;
-                double w[16];
-#pragma unroll
-                for (int h = 0; h < 4; ++h) ldg256(pp + 4 * h, w[4 * h], w[4 * h + 1], w[4 * h + 2], w[4 * h + 3]);
-#pragma unroll
-                for (int i = 0; i < D; ++i) {
-#pragma unroll
-                    for (int j = 0; j < D; ++j) r.As[i][j] = k == 0 ? w[i * 3 + j] : SA_ADD(r.As[i][j], w[i * 3 + j]);
-                    r.bv[k][i] = w[9 + i];
-                    r.cv[k][i] = w[12 + i];
-                    r.bs[i] = k == 0 ? w[9 + i] : SA_ADD(r.bs[i], w[9 + i]);
-                    r.cs[i] = k == 0 ? w[12 + i] : SA_ADD(r.cs[i], w[12 + i]);
-                }
-                r.a0v[k] = w[15];
-                r.a0s = k == 0 ? w[15] : SA_ADD(r.a0s, w[15]);
-            } else {
-#pragma unroll
-                for (int i = 0; i < D; ++i) {
-#pragma unroll
-                    for (int j = 0; j < D; ++j) {
-                        const double t = a.A ? __ldg(a.A + (int64_t)vk * D * D + i * D + j) : a.A_const[i * D + j];
-                        r.As[i][j] = k == 0 ? t : SA_ADD(r.As[i][j], t);
-                    }
-                    const double tb = a.b ? __ldg(a.b + (int64_t)vk * D + i) : 0.0;
-                    const double tc = a.c ? __ldg(a.c + (int64_t)vk * D + i) : 0.0;
-                    r.bv[k][i] = tb;
-                    r.cv[k][i] = tc;
-                    r.bs[i] = k == 0 ? tb : SA_ADD(r.bs[i], tb);
-                    r.cs[i] = k == 0 ? tc : SA_ADD(r.cs[i], tc);
-                }
-                const double t0 = a.a0 ? __ldg(a.a0 + vk) : a.a0_const;
-                r.a0v[k] = t0;
-                r.a0s = k == 0 ? t0 : SA_ADD(r.a0s, t0);
-            }
-        }
-    }
-}
-
-// nodal coefficients only (vertex coordinates already in r.x)
+// nodal coefficients of the element's vertices (r.v loaded)
 template <int D, int OPS>
 __device__ __forceinline__ void element_load_coeffs(const NumArgs &a, ElemRaw<D> &r)
 {
@@ -632,6 +630,16 @@ __device__ __forceinline__ void element_load_coeffs(const NumArgs &a, ElemRaw<D>
             }
         }
     }
+}
+
+template <int D, int OPS>
+__device__ __forceinline__ void element_load2(const NumArgs &a, ElemRaw<D> &r)
+{
+    if constexpr ((OPS & (OP_STIFF | OP_ELASTIC | OP_GENERAL)) != 0) {
+#pragma unroll
+        for (int k = 0; k <= D; ++k) load_vertex<D>((const typename VecT<D>::type *)a.qv, r.v[k], r.x[k]);
+    }
+    element_load_coeffs<D, OPS>(a, r);
 }
 
 // K1: bit-exact gradients and per-element coefficient sums from raw inputs.
@@ -757,17 +765,11 @@ __device__ __forceinline__ void krow_runtime(const NumArgs &a, const ElemGeo<D> 
 // accumulators indexed by the 8-bit column ranks stored with each incidence.
 // Used when a node has more than 31 incidences or the block kernel's shared
 // memory does not fit.
-template <int D, int M, int OPS, int CORE, int ILP, bool XC>
-__global__ void __launch_bounds__(128) k_numeric_rowgather(NumArgs a)
+template <int D, int M, int OPS, int CORE, int ILP, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a)
 {
     constexpr int NOUT = n_outputs<OPS>();
     extern __shared__ double smem_acc[];
-    // XC: the row's neighbour coordinates (and node ids) are cached in the
-    // owner's private shared memory, so an incidence gathers only its record
-    // and volume -- the element's vertices are read from the cache by rank.
-    const int maxdeg = a.acc_stride / (M * M);
-    double *xc = smem_acc + (size_t)NOUT * a.acc_stride * blockDim.x;                 // [maxdeg*D][nthr]
-    int *nidc = reinterpret_cast<int *>(xc + (size_t)maxdeg * D * blockDim.x);        // [maxdeg][nthr]
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int64_t nl = blockIdx.x * (int64_t)blockDim.x + tid;
     int nz[NOUT];
@@ -782,28 +784,7 @@ __global__ void __launch_bounds__(128) k_numeric_rowgather(NumArgs a)
             for (int l = 0; l < M; ++l)
                 for (int k = 0; k < deg_stride; ++k)
                     smem_acc[(o * a.acc_stride + l * row_stride + k) * nthr + tid] = 0.0;
-        if constexpr (XC) {
-            for (int k = 0; k < deg; ++k) {
-                const int node = __ldg(a.cols + c0 + k);
-                double x[D];
-                load_vertex<D>((const typename VecT<D>::type *)a.qv, node, x);
-                nidc[k * nthr + tid] = node;
-#pragma unroll
-                for (int c = 0; c < D; ++c) xc[(k * D + c) * nthr + tid] = x[c];
-            }
-        }
-        auto cached_load = [&](uint2 rec, ElemRaw<D> &r) {
-            r.vol = __ldg(a.vols + (rec.x & 0x3fffffffu));
-#pragma unroll
-            for (int b = 0; b <= D; ++b) {
-                const int rk = (rec.y >> (8 * b)) & 0xff;
-                r.v[b] = nidc[rk * nthr + tid];
-#pragma unroll
-                for (int c = 0; c < D; ++c) r.x[b][c] = xc[(rk * D + c) * nthr + tid];
-            }
-            element_load_coeffs<D, OPS>(a, r);
-        };
-        const int64_t t1 = a.inc_ptr[nl + 1];
+        const int64_t t1 = a.dbg == 3 ? a.inc_ptr[nl] : a.inc_ptr[nl + 1];   // 3: stores only
         int64_t emin = INT64_MAX;
         constexpr int MM = M * M;
         double dsum = 0.0;
@@ -839,31 +820,66 @@ __global__ void __launch_bounds__(128) k_numeric_rowgather(NumArgs a)
                                 vals[(b * NOUT + o) * MM + l * M + n];
             }
         };
-        int64_t t = a.inc_ptr[nl];
-        for (; ILP == 2 && t + 1 < t1; t += 2) {
-            const uint2 r1 = __ldg(a.inc + t), r2 = __ldg(a.inc + t + 1);
-            ElemRaw<D> x1, x2;
-            if constexpr (XC) {
-                cached_load(r1, x1);
-                cached_load(r2, x2);
+        const int64_t t0 = a.inc_ptr[nl];
+        const IncRec *wrec = a.winc ? a.winc + a.wseg[nl >> 5] + (nl & 31) : nullptr;
+        // stage 1 of incidence t: its record, connectivity and volume
+        auto load1 = [&](int64_t t, uint2 &rec, ElemRaw<D> &x) {
+            if (wrec) {
+                unsigned long long u0, u1, u2, u3;
+                asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
+                    : "=l"(u0), "=l"(u1), "=l"(u2), "=l"(u3)
+                    : "l"(wrec + 32 * (t - t0)));
+                rec = make_uint2((unsigned)u0, (unsigned)(u0 >> 32));
+                x.v[0] = (int)(unsigned)u1;
+                if constexpr (D >= 1) x.v[1] = (int)(unsigned)(u1 >> 32);
+                if constexpr (D >= 2) x.v[2] = (int)(unsigned)u2;
+                if constexpr (D >= 3) x.v[3] = (int)(unsigned)(u2 >> 32);
+                x.vol = __longlong_as_double((long long)u3);
             } else {
-                element_load1<D, OPS>(a, r1.x & 0x3fffffffu, x1);
-                element_load1<D, OPS>(a, r2.x & 0x3fffffffu, x2);
-                element_load2<D, OPS>(a, x1);
-                element_load2<D, OPS>(a, x2);
+                rec = __ldg(a.inc + t);
+                element_load1<D, OPS>(a, rec.x & 0x3fffffffu, x);
             }
+        };
+        int64_t t = t0;
+        if constexpr (ILP == 3) {
+            // software pipeline: while incidence t is folded, the vertex /
+            // coefficient gathers of t+1 and the record of t+2 are in flight
+            // (index clamped to the row's last incidence: the tail re-reads it)
+            if (t < t1) {
+                const int64_t last = t1 - 1;
+                uint2 rc, rn;
+                ElemRaw<D> xc, xn;
+                load1(t, rc, xc);
+                load1(min(t + 1, last), rn, xn);
+                element_load2<D, OPS>(a, xc);
+                for (; t < t1; ++t) {
+                    uint2 rnn;
+                    ElemRaw<D> xnn;
+                    load1(min(t + 2, last), rnn, xnn);
+                    element_load2<D, OPS>(a, xn);
+                    fold(xc, rc);
+                    xc = xn;
+                    rc = rn;
+                    xn = xnn;
+                    rn = rnn;
+                }
+            }
+        }
+        for (; ILP == 2 && t + 1 < t1; t += 2) {
+            uint2 r1, r2;
+            ElemRaw<D> x1, x2;
+            load1(t, r1, x1);
+            load1(t + 1, r2, x2);
+            element_load2<D, OPS>(a, x1);
+            element_load2<D, OPS>(a, x2);
             fold(x1, r1);
             fold(x2, r2);
         }
         for (; t < t1; ++t) {
-            const uint2 r1 = __ldg(a.inc + t);
+            uint2 r1;
             ElemRaw<D> x1;
-            if constexpr (XC) {
-                cached_load(r1, x1);
-            } else {
-                element_load1<D, OPS>(a, r1.x & 0x3fffffffu, x1);
-                element_load2<D, OPS>(a, x1);
-            }
+            load1(t, r1, x1);
+            element_load2<D, OPS>(a, x1);
             fold(x1, r1);
         }
         if (emin != INT64_MAX) atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)emin);
@@ -885,15 +901,25 @@ __global__ void __launch_bounds__(128) k_numeric_rowgather(NumArgs a)
         if (uniform) {
             const int64_t base = __shfl_sync(full, active ? a.indptr[M * nl] : (int64_t)0, 0);
             const int run = M * M * d0, mdeg = M * d0;
+            // entry i = lane + 32 it of the warp's run -> (row r, dof row l,
+            // column k), stepped incrementally (no per-entry division)
+            int r = lane / run, j = lane - r * run;
+            int l = j / mdeg, k = j - l * mdeg;
+            const int q32 = 32 / run, r32 = 32 - q32 * run;
+            const int dl = r32 / mdeg, dk = r32 - dl * mdeg;
             for (int i = lane; i < 32 * run; i += 32) {
-                const int r = i / run, j = i - r * run;
-                const int l = j / mdeg, k = j - l * mdeg;
+                const int sidx = (l * row_stride + k) * nthr + wbase + r;
 #pragma unroll
                 for (int o = 0; o < NOUT; ++o) {
-                    const double val = smem_acc[(o * a.acc_stride + l * row_stride + k) * nthr + wbase + r];
+                    const double val = smem_acc[o * a.acc_stride * nthr + sidx];
                     a.vals[o][base + i] = val;
                     nz[o] += (val == 0.0);
                 }
+                k += dk;
+                l += dl;
+                r += q32;
+                if (k >= mdeg) { k -= mdeg; ++l; }
+                if (l >= M) { l -= M; ++r; }
             }
         } else if (active) {
             for (int o = 0; o < NOUT; ++o) {
@@ -1502,6 +1528,21 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
     SA_CUDA_TRY(cudaMemcpyAsync(&md, P->counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     SA_CUDA_TRY(cudaStreamSynchronize(st));
     P->max_deg = md;
+    // warp-interleaved records for the row-gather kernel (SA_WINC=0: off)
+    const char *wi_s = getenv("SA_WINC");
+    if (nn && !(wi_s && atoi(wi_s) == 0)) {
+        const int64_t nw = (nn + 31) / 32;
+        SA_CUDA_TRY(cudaMallocAsync((void **)&P->wseg, (nw + 1) * sizeof(int64_t), st));
+        SA_LAUNCH(k_warp_span, grid_for(nw, 128), 128, 0, st, P->inc_ptr, nn, cnt);
+        SA_TRY(exclusive_scan_i64(cnt, P->wseg, nw, P->scan_tmp, st));
+        SA_CUDA_TRY(cudaMemcpyAsync(&P->n_winc, P->wseg + nw, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        SA_CUDA_TRY(cudaMallocAsync((void **)&P->winc, std::max<int64_t>(P->n_winc, 1) * sizeof(IncRec), st));
+        // padding records (rows shorter than their warp's longest) = all ones: ea = 0xffffffff sentinel
+        SA_CUDA_TRY(cudaMemsetAsync(P->winc, 0xff, std::max<int64_t>(P->n_winc, 1) * sizeof(IncRec), st));
+        SA_LAUNCH(k_winc_fill<D>, grid_for(nn, 128), 128, 0, st, (const I *)M->me, M->vols, P->inc_ptr, P->inc, nn,
+                  P->wseg, P->winc);
+    }
     // fold programs + templates: only for the tile / chunk kernels
     if (want_tile_kernel() || want_chunk_kernel()) {
         std::vector<int64_t> hcp(nn + 1), hip(nn + 1);
@@ -1551,22 +1592,27 @@ template <int D, int M, int OPS, int CORE>
 int launch_rowgather(const NumArgs &a, int64_t nnodes, cudaStream_t st)
 {
     constexpr int NOUT = n_outputs<OPS>();
-    // SA_ILP (1|2): incidences in flight per thread (default 1 in 2D, 2 in 3D);
-    // SA_XCACHE (0|1): neighbour-coordinate cache (default off: slower, measured)
-    const char *ilp_s = getenv("SA_ILP"), *xc_s = getenv("SA_XCACHE");
-    const int ilp = ilp_s ? atoi(ilp_s) : ((D == 3 && !(OPS & OP_GENERAL)) ? 2 : 1);
-    const bool xc = xc_s ? atoi(xc_s) != 0 : false;
-    const int maxdeg = a.acc_stride / (M * M);
-    const size_t per_thread = (size_t)NOUT * a.acc_stride * sizeof(double) +
-                              (xc ? (size_t)maxdeg * (D * sizeof(double) + sizeof(int)) : 0);
+    // SA_ILP (1|2|3): incidences in flight per thread (3 = software
+    // pipeline); SA_MINB (0|6|8): minimum resident 128-thread blocks per SM
+    // the single-incidence kernel is register-capped for (0 = no cap)
+    const char *ilp_s = getenv("SA_ILP"), *mb_s = getenv("SA_MINB");
+    // defaults measured on the BASELINE configs (profiles/r01): the kernel is
+    // latency-bound, so occupancy wins over per-thread ILP except for the
+    // register-heavy elastic operator, which gains from the pipeline
+    const int ilp = ilp_s ? atoi(ilp_s) : (M > 1 ? 3 : 1);
+    const int minb = mb_s ? atoi(mb_s) : ((D <= 2 && M == 1 && !(OPS & OP_GENERAL)) ? 8 : 0);
+    const size_t per_thread = (size_t)NOUT * a.acc_stride * sizeof(double);
     int block = 128;
     while (per_thread * block > 100 * 1024 && block > 32) block /= 2;
     const size_t smem = per_thread * block;
     if (smem > 200 * 1024)
         return set_error(SA_ERR_CAPACITY, "row accumulators need %zu B of shared memory per %d threads", smem, block);
     void (*kern)(NumArgs);
-    if (xc) kern = ilp == 2 ? k_numeric_rowgather<D, M, OPS, CORE, 2, true> : k_numeric_rowgather<D, M, OPS, CORE, 1, true>;
-    else kern = ilp == 2 ? k_numeric_rowgather<D, M, OPS, CORE, 2, false> : k_numeric_rowgather<D, M, OPS, CORE, 1, false>;
+    if (ilp == 2) kern = k_numeric_rowgather<D, M, OPS, CORE, 2, 1>;
+    else if (ilp == 3) kern = k_numeric_rowgather<D, M, OPS, CORE, 3, 1>;
+    else if (minb == 8) kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 8>;
+    else if (minb == 6) kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 6>;
+    else kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 1>;
     SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (nnodes) SA_LAUNCH(kern, grid_for(nnodes, block), block, smem, st, a);
     return SA_OK;
@@ -1644,6 +1690,7 @@ template <int D, int M, int OPS, int CORE>
 int launch_numeric(const sa_plan *P, const NumArgs &a, cudaStream_t st)
 {
     if (P->ck_ok && want_chunk_kernel()) SA_TRY_OR_FALL(launch_chunks<D, M, OPS, CORE>(P, a, st));
+
     const int64_t nnodes = P->nnodes;
     const bool use_tile = P->tm_ok && want_tile_kernel();
     if (use_tile) {
@@ -1802,7 +1849,7 @@ int sa_mesh_destroy(sa_mesh *M)
 int sa_plan_destroy(sa_plan *P)
 {
     if (!P) return SA_OK;
-    free_all({P->inc_ptr, P->inc, P->colptr, P->cols, P->indptr, P->indices, P->counters, P->scan_tmp, P->inc_e,
+    free_all({P->inc_ptr, P->inc, P->winc, P->wseg, P->colptr, P->cols, P->indptr, P->indices, P->counters, P->scan_tmp, P->inc_e,
               P->fold, P->tile_e0, P->tile_tm, P->tm_off, P->tm, P->ck_tm, P->ck_pb, P->ck_tm_off, P->ck_tmw,
               P->ck_flags, P->ck_rs});
     delete P;
@@ -1887,7 +1934,7 @@ int sa_numeric(sa_plan *P, int ops, const sa_coeffs *cf, double *const *vals_dev
     memset(&a, 0, sizeof a);
     a.qv = M->qv; a.me = M->me; a.vols = M->vols;
     a.nnodes = P->nnodes; a.node_begin = P->node_begin;
-    a.inc_ptr = P->inc_ptr; a.inc = P->inc; a.colptr = P->colptr; a.indptr = P->indptr; a.cols = P->cols;
+    a.inc_ptr = P->inc_ptr; a.inc = P->inc; a.winc = P->winc; a.wseg = P->wseg; a.colptr = P->colptr; a.indptr = P->indptr; a.cols = P->cols;
     a.dbg = getenv("SA_DBG") ? atoi(getenv("SA_DBG")) : 0;
     a.acc_stride = (int)(P->m * P->m * std::max<int64_t>(P->max_deg, 1));
     int nout = 0;

@@ -1,10 +1,8 @@
 #!/bin/bash
-# numeric-phase sweep over tile lanes per config (no profiler)
+# usage: sweep.sh "CFG:ENV=..;ENV=.. CFG:..."   -- one bench line per case
 cd "${GRAFT_REPO_ROOT:-$(dirname $0)/..}"
-mkdir -p gpurun_out
-for c in ${CONFIGS:-C2 C3}; do
-  for L in ${LANES:-1 2 4 8}; do
-    SA_TILE_LANES=$L timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/sweep_${c}_L$L.log 2>&1
-    python -c "import json,sys; d=json.loads(open('gpurun_out/sweep_${c}_L$L.log').read().strip().splitlines()[-1]); print('$c', 'L=$L', round(d['ms_per_step'],4), 'ms', round(d['roofline']['frac'],3))" 2>/dev/null || (echo "$c L=$L failed"; tail -3 gpurun_out/sweep_${c}_L$L.log)
-  done
+for case in "$@"; do
+  cfg=${case%%:*}; envs=${case#*:}
+  env $(echo $envs | tr ';' ' ') timeout 900 python bench.py --config $cfg --steps ${STEPS:-5} --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | grep '"metric"' | \
+    python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$cfg', '$envs', round(d['ms_per_step'],3), round(d['roofline']['frac'],4))"
 done
