@@ -9,6 +9,8 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/ev_s
 timeout 900 python bench.py > gpurun_out/ev_bench_C2.log 2>&1; echo "bench rc=$?" >> gpurun_out/ev_bench_C2.log
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/ev_bench_ref.log 2>&1
 for c in C1 C3 C4; do timeout 600 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/ev_bench_$c.log 2>&1; done
+timeout 900 python bench.py --config C5 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/ev_bench_C5.log 2>&1
+timeout 1800 python tools/fullsize_parity.py C1 C2 C3 C4 C5 > gpurun_out/ev_fullsize_parity.log 2>&1; echo "parity rc=$?" >> gpurun_out/ev_fullsize_parity.log
 CMD="python bench.py --config C2 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/ev_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ev_launches_C2.csv $CMD > gpurun_out/ev_ncu1.log 2>&1 && \
