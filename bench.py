@@ -49,6 +49,27 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
+def profiled_traffic(name):
+    """DRAM bytes (read + write) per launch of the numeric kernel for this
+    config, from the newest committed ncu --set full summary
+    (profiles/rNN/ncu_<config>_*.json, written by tools/ncu_summary.py);
+    null when no capture exists for the default kernel."""
+    import glob
+
+    if os.environ.get("SA_KERNEL") or os.environ.get("SA_BENCH_RENUMBER"):
+        return {"traffic": None}
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"ncu_{name}_*.json")))
+    if not paths:
+        return {"traffic": None}
+    try:
+        with open(paths[-1]) as f:
+            d = json.load(f)
+        return {"traffic": float(d["dram_bytes"]), "traffic_source": os.path.relpath(paths[-1], ROOT),
+                "traffic_kernel_ms": float(d["duration_ns"]) * 1e-6}
+    except Exception:
+        return {"traffic": None}
+
+
 def make_mesh(cfg, vols_on_device=True):
     import paper_1401_3301_b200 as P
 
@@ -335,14 +356,16 @@ def main():
         "config": {"workload": args.config, **config_desc(cfg), "nq": nq, "nme": nme,
                    "nnz_structural_per_matrix": nnz_struct_all, "n_out": len(kernels),
                    "exact_zero_entries": zeros, "parallelism": f"row-blocks x{world}",
-                   "plan": plan.stats(), "kernel": os.environ.get("SA_KERNEL", "default"),
+                   "plan": {k: v for k, v in plan.stats().items()
+                            if k in ("incidences", "max_row_nodes", "nodes", "nnz") or v},
+                   "kernel": os.environ.get("SA_KERNEL", "default"),
                    "l2": "flushed between timed steps (256 MiB write); inputs+outputs > L2",
                    "timing": "per-step CUDA events on the launching stream, summed; max over ranks"},
         "nnz_per_s": nnz_struct_all * len(kernels) / (ms_per_step * 1e-3),
         "symbolic_ms": t_sym_ms,
         "numeric_ms": ms_per_step,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "frac": achieved / peak, **profiled_traffic(args.config), "peak_kind": peak_kind,
                      "algorithmic_bytes": b_num, "kernel": {"chunk": "k_numeric_chunks", "tile": "k_numeric_tiles"}.get(
                          os.environ.get("SA_KERNEL", ""), "k_numeric_rowgather"),
                      "frac_of_8TBps_nominal": achieved / 8000.0},
