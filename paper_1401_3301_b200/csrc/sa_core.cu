@@ -770,20 +770,33 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a)
 {
     constexpr int NOUT = n_outputs<OPS>();
     extern __shared__ double smem_acc[];
-    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int tid = threadIdx.x, lane = tid & 31;
     const int64_t nl = blockIdx.x * (int64_t)blockDim.x + tid;
+    // Accumulators: per warp and output a plane of 32 lane rows of S doubles;
+    // lane j's dof row l, column k at wacc[o*32*S + j*S + l*M*deg + k].  When
+    // the warp's rows all have degree d0, S = M*M*d0 and the plane IS the
+    // warp's CSR run (row-major, consecutive rows), so the store phase is a
+    // straight coalesced copy; otherwise S is padded to the warp's largest
+    // row (odd, so lane strides hit distinct banks) and rows store their own
+    // segments.
+    const unsigned full = 0xffffffffu;
+    const bool active = nl < a.nnodes;
+    const int64_t c0 = active ? a.colptr[nl] : 0;
+    const int deg = active ? (int)(a.colptr[nl + 1] - c0) : -1;
+    const int d0 = __shfl_sync(full, deg, 0);
+    const bool uniform = __all_sync(full, deg == d0) && d0 > 0;
+    int dmax = deg;
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) dmax = max(dmax, __shfl_xor_sync(full, dmax, sh));
+    const int S = uniform ? M * M * d0 : ((M * M * max(dmax, 0)) | 1);
+    double *wacc = smem_acc + (size_t)(tid >> 5) * NOUT * 32 * (a.acc_stride | 1) + lane * S;
     int nz[NOUT];
 #pragma unroll
     for (int o = 0; o < NOUT; ++o) nz[o] = 0;
-    if (nl < a.nnodes) {
-        const int64_t c0 = a.colptr[nl];
-        const int deg = (int)(a.colptr[nl + 1] - c0);
+    if (active) {
         const int deg_stride = M * deg;
-        const int row_stride = a.acc_stride / M;
         for (int o = 0; o < NOUT; ++o)
-            for (int l = 0; l < M; ++l)
-                for (int k = 0; k < deg_stride; ++k)
-                    smem_acc[(o * a.acc_stride + l * row_stride + k) * nthr + tid] = 0.0;
+            for (int k = 0; k < M * deg_stride; ++k) wacc[o * 32 * S + k] = 0.0;
         const int64_t t1 = a.dbg == 3 ? a.inc_ptr[nl] : a.inc_ptr[nl + 1];   // 3: stores only
         int64_t emin = INT64_MAX;
         constexpr int MM = M * M;
@@ -816,8 +829,7 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a)
                     for (int l = 0; l < M; ++l)
 #pragma unroll
                         for (int n = 0; n < M; ++n)
-                            smem_acc[(o * a.acc_stride + l * row_stride + r * M + n) * nthr + tid] +=
-                                vals[(b * NOUT + o) * MM + l * M + n];
+                            wacc[o * 32 * S + l * deg_stride + r * M + n] += vals[(b * NOUT + o) * MM + l * M + n];
             }
         };
         const int64_t t0 = a.inc_ptr[nl];
@@ -883,54 +895,30 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a)
             fold(x1, r1);
         }
         if (emin != INT64_MAX) atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)emin);
-        if (a.dbg) smem_acc[tid] = dsum;
+        if (a.dbg) wacc[0] = dsum;
     }
-    // Stores.  When the warp's 32 rows all have the same degree (every warp
-    // inside a structured mesh), their CSR segments form one contiguous run
-    // and the warp writes it coalesced from the owners' accumulators;
-    // otherwise each owner writes its own row segment.
+    // Stores (see the accumulator layout above)
     __syncwarp();
-    {
-        const unsigned full = 0xffffffffu;
-        const int lane = tid & 31, wbase = tid & ~31;
-        const bool active = nl < a.nnodes;
-        const int mydeg = active ? (int)(a.colptr[nl + 1] - a.colptr[nl]) : -1;
-        const int d0 = __shfl_sync(full, mydeg, 0);
-        const bool uniform = __all_sync(full, mydeg == d0) && d0 > 0;
-        const int row_stride = a.acc_stride / M;
-        if (uniform) {
-            const int64_t base = __shfl_sync(full, active ? a.indptr[M * nl] : (int64_t)0, 0);
-            const int run = M * M * d0, mdeg = M * d0;
-            // entry i = lane + 32 it of the warp's run -> (row r, dof row l,
-            // column k), stepped incrementally (no per-entry division)
-            int r = lane / run, j = lane - r * run;
-            int l = j / mdeg, k = j - l * mdeg;
-            const int q32 = 32 / run, r32 = 32 - q32 * run;
-            const int dl = r32 / mdeg, dk = r32 - dl * mdeg;
-            for (int i = lane; i < 32 * run; i += 32) {
-                const int sidx = (l * row_stride + k) * nthr + wbase + r;
+    if (uniform) {
+        const int64_t base = __shfl_sync(full, active ? a.indptr[M * nl] : (int64_t)0, 0);
+        const double *plane = wacc - lane * S;
+        for (int i = lane; i < 32 * S; i += 32) {
 #pragma unroll
-                for (int o = 0; o < NOUT; ++o) {
-                    const double val = smem_acc[o * a.acc_stride * nthr + sidx];
-                    a.vals[o][base + i] = val;
-                    nz[o] += (val == 0.0);
-                }
-                k += dk;
-                l += dl;
-                r += q32;
-                if (k >= mdeg) { k -= mdeg; ++l; }
-                if (l >= M) { l -= M; ++r; }
-            }
-        } else if (active) {
             for (int o = 0; o < NOUT; ++o) {
-                double *out = a.vals[o];
-                for (int l = 0; l < M; ++l) {
-                    const int64_t p = a.indptr[M * nl + l];
-                    for (int k = 0; k < M * mydeg; ++k) {
-                        const double val = smem_acc[(o * a.acc_stride + l * row_stride + k) * nthr + tid];
-                        out[p + k] = val;
-                        nz[o] += (val == 0.0);
-                    }
+                const double val = plane[o * 32 * S + i];
+                a.vals[o][base + i] = val;
+                nz[o] += (val == 0.0);
+            }
+        }
+    } else if (active) {
+        for (int o = 0; o < NOUT; ++o) {
+            double *out = a.vals[o];
+            for (int l = 0; l < M; ++l) {
+                const int64_t p = a.indptr[M * nl + l];
+                for (int k = 0; k < M * deg; ++k) {
+                    const double val = wacc[o * 32 * S + l * M * deg + k];
+                    out[p + k] = val;
+                    nz[o] += (val == 0.0);
                 }
             }
         }
@@ -1596,15 +1584,15 @@ int launch_rowgather(const NumArgs &a, int64_t nnodes, cudaStream_t st)
 {
     constexpr int NOUT = n_outputs<OPS>();
     // SA_ILP (1|2|3): incidences in flight per thread (3 = software
-    // pipeline); SA_MINB (0|6|8): minimum resident 128-thread blocks per SM
+    // pipeline); SA_MINB (0|3|6|8): minimum resident 128-thread blocks per SM
     // the single-incidence kernel is register-capped for (0 = no cap)
     const char *ilp_s = getenv("SA_ILP"), *mb_s = getenv("SA_MINB");
     // defaults measured on the BASELINE configs (profiles/r01): the kernel is
     // latency-bound, so occupancy wins over per-thread ILP except for the
     // register-heavy elastic operator, which gains from the pipeline
     const int ilp = ilp_s ? atoi(ilp_s) : (M > 1 ? 3 : 1);
-    const int minb = mb_s ? atoi(mb_s) : ((D <= 2 && M == 1 && !(OPS & OP_GENERAL)) ? 8 : 0);
-    const size_t per_thread = (size_t)NOUT * a.acc_stride * sizeof(double);
+    const int minb = mb_s ? atoi(mb_s) : (M > 1 ? 0 : (OPS & OP_GENERAL) ? 3 : (D <= 2 ? 8 : 6));
+    const size_t per_thread = (size_t)NOUT * (a.acc_stride | 1) * sizeof(double);
     int block = 128;
     while (per_thread * block > 100 * 1024 && block > 32) block /= 2;
     const size_t smem = per_thread * block;
@@ -1615,6 +1603,7 @@ int launch_rowgather(const NumArgs &a, int64_t nnodes, cudaStream_t st)
     else if (ilp == 3) kern = k_numeric_rowgather<D, M, OPS, CORE, 3, 1>;
     else if (minb == 8) kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 8>;
     else if (minb == 6) kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 6>;
+    else if (minb == 3) kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 3>;
     else kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 1>;
     SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (nnodes) SA_LAUNCH(kern, grid_for(nnodes, block), block, smem, st, a);
