@@ -783,6 +783,10 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a)
     const bool active = nl < a.nnodes;
     const int64_t c0 = active ? a.colptr[nl] : 0;
     const int deg = active ? (int)(a.colptr[nl + 1] - c0) : -1;
+    // the row's CSR base, loaded with the degree (independent loads: one
+    // round trip) rather than after the incidence loop
+    const int64_t row_base = active ? a.indptr[M * nl] : 0;
+    const int64_t inc0 = active ? a.inc_ptr[nl] : 0, inc1 = active ? a.inc_ptr[nl + 1] : 0;
     const int d0 = __shfl_sync(full, deg, 0);
     const bool uniform = __all_sync(full, deg == d0) && d0 > 0;
     int dmax = deg;
@@ -797,7 +801,7 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a)
         const int deg_stride = M * deg;
         for (int o = 0; o < NOUT; ++o)
             for (int k = 0; k < M * deg_stride; ++k) wacc[o * 32 * S + k] = 0.0;
-        const int64_t t1 = a.dbg == 3 ? a.inc_ptr[nl] : a.inc_ptr[nl + 1];   // 3: stores only
+        const int64_t t1 = a.dbg >= 3 ? inc0 : inc1;   // 3: stores only, 4: neither
         int64_t emin = INT64_MAX;
         constexpr int MM = M * M;
         double dsum = 0.0;
@@ -832,7 +836,7 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a)
                             wacc[o * 32 * S + l * deg_stride + r * M + n] += vals[(b * NOUT + o) * MM + l * M + n];
             }
         };
-        const int64_t t0 = a.inc_ptr[nl];
+        const int64_t t0 = inc0;
         const IncRec *wrec = a.winc ? a.winc + a.wseg[nl >> 5] + (nl & 31) : nullptr;
         // stage 1 of incidence t: its record, connectivity and volume
         auto load1 = [&](int64_t t, uint2 &rec, ElemRaw<D> &x) {
@@ -899,8 +903,9 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a)
     }
     // Stores (see the accumulator layout above)
     __syncwarp();
-    if (uniform) {
-        const int64_t base = __shfl_sync(full, active ? a.indptr[M * nl] : (int64_t)0, 0);
+    if (a.dbg == 4) {   // diagnostics: metadata + zero-init only, no stores
+    } else if (uniform) {
+        const int64_t base = __shfl_sync(full, row_base, 0);
         const double *plane = wacc - lane * S;
         for (int i = lane; i < 32 * S; i += 32) {
 #pragma unroll
