@@ -87,6 +87,12 @@ struct sa_plan {
     int64_t ck_nrec = 0;
     int64_t ck_maxw = 0;           // largest chunk template (words)
     unsigned ck_epoch = 0;         // bumped per launch
+    // two-pass numeric ("element rows"): incidence slot of every (element, alpha)
+    // of the block's element range, and the per-incidence local-row buffer
+    uint4 *epos = nullptr;         // (e_hi - e_lo): slot t of (e, alpha) in inc, or ~0u
+    int64_t e_lo = 0, e_hi = 0;
+    double *kbuf = nullptr;        // (n_inc * kbuf_stride) local rows in incidence order
+    int64_t kbuf_elems = 0;
 };
 
 // numeric-phase arguments (shared by the per-dimension translation units)
@@ -114,6 +120,10 @@ struct NumArgs {
     const double *A; const double *b; const double *c; const double *a0;
     double A_const[9]; double a0_const;
     const double *gen_packed;  // (nq, 16) AoS [A(9) b(3) c(3) a0] or NULL
+    // two-pass numeric: element pass writes local rows to kbuf (stride kstride
+    // doubles per incidence), the ordered fold pass reads them
+    double *kbuf; int kstride;
+    const uint4 *epos; int64_t e_lo, ne;
     double mass_coef_diag, mass_coef_off;  // 2/((d+1)(d+2)(d+3)), 1/(...) as Python computes them
     double mass_wc;  // constant weight: (wsum + w) + w, the same for every (alpha, beta)
 };
@@ -765,7 +775,7 @@ __device__ __forceinline__ void krow_runtime(const NumArgs &a, const ElemGeo<D> 
 // accumulators indexed by the 8-bit column ranks stored with each incidence.
 // Used when a node has more than 31 incidences or the block kernel's shared
 // memory does not fit.
-template <int D, int M, int OPS, int CORE, int ILP, int MINB>
+template <int D, int M, int OPS, int CORE, int ILP, int MINB, bool PRE = false>
 __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a)
 {
     constexpr int NOUT = n_outputs<OPS>();
@@ -805,6 +815,22 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a)
         int64_t emin = INT64_MAX;
         constexpr int MM = M * M;
         double dsum = 0.0;
+        constexpr int VPR = (D + 1) * NOUT * MM;
+        // fold one local row set into the row accumulators (ranks: 8-bit
+        // column rank of each element vertex within this row)
+        auto accum = [&](const double(&vals)[VPR], unsigned ranks) {
+#pragma unroll
+            for (int b = 0; b <= D; ++b) {
+                const int r = (ranks >> (8 * b)) & 0xff;
+#pragma unroll
+                for (int o = 0; o < NOUT; ++o)
+#pragma unroll
+                    for (int l = 0; l < M; ++l)
+#pragma unroll
+                        for (int n = 0; n < M; ++n)
+                            wacc[o * 32 * S + l * deg_stride + r * M + n] += vals[(b * NOUT + o) * MM + l * M + n];
+            }
+        };
         auto fold = [&](const ElemRaw<D> &x, uint2 rec) {
             if (a.dbg == 1) {   // diagnostics: memory traffic only
 #pragma unroll
@@ -824,17 +850,7 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a)
                 for (int i = 0; i < (D + 1) * NOUT * MM; ++i) dsum += vals[i];
                 return;
             }
-#pragma unroll
-            for (int b = 0; b <= D; ++b) {
-                const int r = (rec.y >> (8 * b)) & 0xff;
-#pragma unroll
-                for (int o = 0; o < NOUT; ++o)
-#pragma unroll
-                    for (int l = 0; l < M; ++l)
-#pragma unroll
-                        for (int n = 0; n < M; ++n)
-                            wacc[o * 32 * S + l * deg_stride + r * M + n] += vals[(b * NOUT + o) * MM + l * M + n];
-            }
+            accum(vals, rec.y);
         };
         const int64_t t0 = inc0;
         const IncRec *wrec = a.winc ? a.winc + a.wseg[nl >> 5] + (nl & 31) : nullptr;
@@ -857,7 +873,46 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a)
             }
         };
         int64_t t = t0;
-        if constexpr (ILP == 3) {
+        if constexpr (PRE) {
+            // two-pass fold: the element pass left this incidence's local
+            // row(s) at kbuf[t * kstride]; records and rows are independent
+            // loads (no dependent gather chain), ILP incidences in flight
+            auto loadk = [&](int64_t tt, double(&v)[VPR]) {
+                const double *src = a.kbuf + tt * a.kstride;
+                if constexpr (VPR % 4 == 0) {
+#pragma unroll
+                    for (int i = 0; i < VPR; i += 4) ldg256(src + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+                } else if constexpr (VPR % 2 == 0) {
+#pragma unroll
+                    for (int i = 0; i < VPR; i += 2) {
+                        const double2 w = __ldg((const double2 *)(src + i));
+                        v[i] = w.x;
+                        v[i + 1] = w.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < VPR; ++i) v[i] = __ldg(src + i);
+                }
+            };
+            constexpr int U = ILP < 1 ? 1 : ILP;
+            for (; t + U <= t1; t += U) {
+                unsigned rk[U];
+                double v[U][VPR];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    rk[u] = __ldg(&a.inc[t + u].y);
+                    loadk(t + u, v[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) accum(v[u], rk[u]);
+            }
+            for (; t < t1; ++t) {
+                double v[VPR];
+                const unsigned rk = __ldg(&a.inc[t].y);
+                loadk(t, v);
+                accum(v, rk);
+            }
+        } else if constexpr (ILP == 3) {
             // software pipeline: while incidence t is folded, the vertex /
             // coefficient gathers of t+1 and the record of t+2 are in flight
             // (index clamped to the row's last incidence: the tail re-reads it)
@@ -881,7 +936,7 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a)
                 }
             }
         }
-        for (; ILP == 2 && t + 1 < t1; t += 2) {
+        for (; !PRE && ILP == 2 && t + 1 < t1; t += 2) {
             uint2 r1, r2;
             ElemRaw<D> x1, x2;
             load1(t, r1, x1);
@@ -891,7 +946,7 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a)
             fold(x1, r1);
             fold(x2, r2);
         }
-        for (; t < t1; ++t) {
+        for (; !PRE && t < t1; ++t) {
             uint2 r1;
             ElemRaw<D> x1;
             load1(t, r1, x1);
@@ -935,6 +990,93 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a)
         for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
         if ((tid & 31) == 0 && v) atomicAdd((unsigned long long *)(a.counters + o), (unsigned long long)v);
     }
+}
+
+// ---------------------------------------------------------------------------
+// Two-pass numeric ("element rows"): pass 1 computes every element of the
+// block ONCE (geometry + all its local rows the block owns) and writes each
+// local row to the slot of its incidence; pass 2 is the row-gather fold
+// (k_numeric_rowgather<PRE = true>) streaming those rows in ascending element
+// order.  Same per-element arithmetic, same fold order: bitwise the one-pass
+// result.  Pays 2 x (local row bytes) of HBM traffic per incidence to save
+// (d+1)-fold recomputation and the per-incidence gathers of vertex
+// coordinates and nodal coefficients (the general operator's 4 x 128 B).
+
+// 256-bit store (sm_100)
+__device__ __forceinline__ void st256(double *p, double a, double b, double c, double d)
+{
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
+template <int D, int M, int OPS, int A = 0>
+__device__ __forceinline__ void element_rows_store(const NumArgs &a, const ElemGeo<D> &g, const unsigned (&pos)[4])
+{
+    constexpr int VPR = (D + 1) * n_outputs<OPS>() * M * M;
+    if (pos[A] != 0xffffffffu) {
+        double vals[VPR];
+        element_krow<D, M, OPS, A>(a, g, vals);
+        double *dst = a.kbuf + (int64_t)pos[A] * a.kstride;
+        if constexpr (VPR % 4 == 0) {
+#pragma unroll
+            for (int i = 0; i < VPR; i += 4) st256(dst + i, vals[i], vals[i + 1], vals[i + 2], vals[i + 3]);
+        } else if constexpr (VPR % 2 == 0) {
+#pragma unroll
+            for (int i = 0; i < VPR; i += 2) *(double2 *)(dst + i) = make_double2(vals[i], vals[i + 1]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < VPR; ++i) dst[i] = vals[i];
+        }
+    }
+    if constexpr (A < D) element_rows_store<D, M, OPS, A + 1>(a, g, pos);
+}
+
+template <int D, int M, int OPS, int CORE>
+__global__ void __launch_bounds__(128) k_element_rows(NumArgs a)
+{
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= a.ne) return;
+    const uint4 p = __ldg(a.epos + i);
+    const unsigned pos[4] = {p.x, p.y, p.z, p.w};
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k <= D; ++k) any |= pos[k] != 0xffffffffu;
+    if (!any) return;   // element does not touch the block
+    const int64_t e = a.e_lo + i;
+    ElemRaw<D> x;
+    element_load1<D, OPS>(a, e, x);
+    element_load2<D, OPS>(a, x);
+    ElemGeo<D> g;
+    if (element_compute<D, OPS, CORE>(x, g)) atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)e);
+    element_rows_store<D, M, OPS>(a, g, pos);
+}
+
+// element range of the block's incidences: out[0] = min e, out[1] = max e
+__global__ void k_inc_erange(const uint2 *__restrict__ inc, int64_t n, unsigned long long *out)
+{
+    unsigned lo = 0xffffffffu, hi = 0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned e = inc[t].x & 0x3fffffffu;
+        lo = min(lo, e);
+        hi = max(hi, e);
+    }
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, sh));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, sh));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(out, (unsigned long long)lo);
+        atomicMax(out + 1, (unsigned long long)hi);
+    }
+}
+
+// slot of (e, alpha): epos[e - e_lo].alpha = t
+__global__ void k_epos_fill(const uint2 *__restrict__ inc, int64_t n, unsigned e_lo, unsigned *__restrict__ epos)
+{
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const unsigned x = inc[t].x;
+    epos[(int64_t)((x & 0x3fffffffu) - e_lo) * 4 + (x >> 30)] = (unsigned)t;
 }
 
 // element lane: local row A of the element -> scatter into the fold array
@@ -1684,8 +1826,31 @@ int launch_chunks(const sa_plan *P, const NumArgs &a, cudaStream_t st)
 }
 
 template <int D, int M, int OPS, int CORE>
+int launch_twopass(const NumArgs &a, int64_t nnodes, cudaStream_t st)
+{
+    constexpr int NOUT = n_outputs<OPS>();
+    if (a.ne) SA_LAUNCH((k_element_rows<D, M, OPS, CORE>), grid_for(a.ne, 128), 128, 0, st, a);
+    const char *ilp_s = getenv("SA_ILP");
+    const int ilp = ilp_s ? atoi(ilp_s) : 2;
+    const size_t per_thread = (size_t)NOUT * (a.acc_stride | 1) * sizeof(double);
+    int block = 128;
+    while (per_thread * block > 100 * 1024 && block > 32) block /= 2;
+    const size_t smem = per_thread * block;
+    if (smem > 200 * 1024)
+        return set_error(SA_ERR_CAPACITY, "row accumulators need %zu B of shared memory per %d threads", smem, block);
+    void (*kern)(NumArgs);
+    if (ilp >= 4) kern = k_numeric_rowgather<D, M, OPS, CORE, 4, 1, true>;
+    else if (ilp == 2 || ilp == 3) kern = k_numeric_rowgather<D, M, OPS, CORE, 2, 1, true>;
+    else kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 1, true>;
+    SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (nnodes) SA_LAUNCH(kern, grid_for(nnodes, block), block, smem, st, a);
+    return SA_OK;
+}
+
+template <int D, int M, int OPS, int CORE>
 int launch_numeric(const sa_plan *P, const NumArgs &a, cudaStream_t st)
 {
+    if (a.kbuf) return launch_twopass<D, M, OPS, CORE>(a, P->nnodes, st);
     if (P->ck_ok && want_chunk_kernel()) SA_TRY_OR_FALL(launch_chunks<D, M, OPS, CORE>(P, a, st));
 
     const int64_t nnodes = P->nnodes;
@@ -1848,7 +2013,7 @@ int sa_plan_destroy(sa_plan *P)
     if (!P) return SA_OK;
     free_all({P->inc_ptr, P->inc, P->winc, P->wseg, P->colptr, P->cols, P->indptr, P->indices, P->counters, P->scan_tmp, P->inc_e,
               P->fold, P->tile_e0, P->tile_tm, P->tm_off, P->tm, P->ck_tm, P->ck_pb, P->ck_tm_off, P->ck_tmw,
-              P->ck_flags, P->ck_rs});
+              P->ck_flags, P->ck_rs, P->epos, P->kbuf});
     delete P;
     return SA_OK;
 }
@@ -1918,6 +2083,51 @@ int sa_plan_pattern(const sa_plan *P, int64_t *indptr_dev, int32_t *indices_dev,
     return SA_OK;
 }
 
+// two-pass numeric ("element rows"): SA_KERNEL=twopass|rowgather forces it
+// on/off; by default it serves the operators where it measured faster
+static bool want_twopass(int ops, int d, int m)
+{
+    const char *k = getenv("SA_KERNEL");
+    if (k && *k) return strcmp(k, "twopass") == 0;
+    (void)m;
+    return ops == SA_OP_GENERAL && d == 3;
+}
+
+// element range, slot map and row buffer of a plan's two-pass numeric phase
+// (built on first use, kept with the plan)
+static int ensure_twopass(sa_plan *P, int64_t kelems, cudaStream_t st)
+{
+    if (!P->epos) {
+        unsigned long long h[2] = {0xffffffffull, 0};
+        unsigned long long *dr = nullptr;
+        SA_CUDA_TRY(cudaMallocAsync((void **)&dr, 2 * sizeof(unsigned long long), st));
+        SA_CUDA_TRY(cudaMemcpyAsync(dr, h, sizeof h, cudaMemcpyHostToDevice, st));
+        if (P->n_inc)
+            SA_LAUNCH(k_inc_erange, std::min<int64_t>(grid_for(P->n_inc, 256), 148 * 8), 256, 0, st, P->inc,
+                      P->n_inc, dr);
+        SA_CUDA_TRY(cudaMemcpyAsync(h, dr, sizeof h, cudaMemcpyDeviceToHost, st));
+        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        SA_CUDA_TRY(cudaFreeAsync(dr, st));
+        P->e_lo = P->n_inc ? (int64_t)h[0] : 0;
+        P->e_hi = P->n_inc ? (int64_t)h[1] + 1 : 0;
+        const int64_t ne = P->e_hi - P->e_lo;
+        SA_CUDA_TRY(cudaMallocAsync((void **)&P->epos, std::max<int64_t>(ne, 1) * sizeof(uint4), st));
+        SA_CUDA_TRY(cudaMemsetAsync(P->epos, 0xff, std::max<int64_t>(ne, 1) * sizeof(uint4), st));
+        if (P->n_inc)
+            SA_LAUNCH(k_epos_fill, grid_for(P->n_inc, 256), 256, 0, st, P->inc, P->n_inc, (unsigned)P->e_lo,
+                      (unsigned *)P->epos);
+    }
+    if (P->kbuf_elems < kelems) {
+        if (P->kbuf) SA_CUDA_TRY(cudaFreeAsync(P->kbuf, st));
+        P->kbuf = nullptr;
+        P->kbuf_elems = 0;
+        if (cudaMallocAsync((void **)&P->kbuf, std::max<int64_t>(kelems, 1) * sizeof(double), st) != cudaSuccess)
+            return set_error(SA_ERR_NOMEM, "two-pass row buffer (%lld doubles) does not fit", (long long)kelems);
+        P->kbuf_elems = kelems;
+    }
+    return SA_OK;
+}
+
 int sa_numeric(sa_plan *P, int ops, const sa_coeffs *cf, double *const *vals_dev, int64_t *n_zero_out, void *stream)
 {
     if (!P || !vals_dev) return set_error(SA_ERR_ARG, "plan/vals is NULL");
@@ -1955,6 +2165,16 @@ int sa_numeric(sa_plan *P, int ops, const sa_coeffs *cf, double *const *vals_dev
         double ws = a.w_const;
         for (int k = 1; k <= d; ++k) ws = ws + a.w_const;
         a.mass_wc = (ws + a.w_const) + a.w_const;
+    }
+    if (want_twopass(ops, d, P->m) && P->n_inc < 0xffffffffLL) {
+        const int vpr = (d + 1) * nout * P->m * P->m;
+        const int ks = vpr;   // row alignment follows from the row size (see loadk)
+        SA_TRY(ensure_twopass(P, (int64_t)ks * P->n_inc, st));
+        a.kbuf = P->kbuf;
+        a.kstride = ks;
+        a.epos = P->epos;
+        a.e_lo = P->e_lo;
+        a.ne = P->e_hi - P->e_lo;
     }
     SA_CUDA_TRY(cudaMemsetAsync(P->counters, 0, 4 * sizeof(int64_t), st));
     SA_CUDA_TRY(cudaMemsetAsync(P->counters + 4, 0x7f, sizeof(int64_t), st));

@@ -75,7 +75,9 @@ def test_elastic_vs_oracle(cuda_ok):
     assert_csr_equal(got, *_oracle(mesh, "elastic", lamb=lam, mu=mu))
 
 
-def test_general_vs_oracle(cuda_ok):
+@pytest.mark.parametrize("kernel", ["rowgather", "twopass"])
+def test_general_vs_oracle(cuda_ok, kernel, monkeypatch):
+    monkeypatch.setenv("SA_KERNEL", kernel)
     mesh = _jittered(3, 20, 14013305)
     nq = mesh.q.shape[1]
     rng = np.random.default_rng(14013305)
@@ -97,10 +99,12 @@ def test_general_reduces_to_stiffness_and_mass(cuda_ok):
     assert_csr_equal(g2, m.row_ptr, m.col_idx, m.vals)
 
 
-def test_row_blocks_stitch_bitwise(cuda_ok):
+@pytest.mark.parametrize("kernel", ["rowgather", "twopass"])
+def test_row_blocks_stitch_bitwise(cuda_ok, kernel, monkeypatch):
     from paper_1401_3301_b200 import parallel
     from paper_1401_3301_b200.device import DeviceMesh
 
+    monkeypatch.setenv("SA_KERNEL", kernel)
     mesh = _jittered(3, 18, 9)
     full = P.assemble_b200(mesh, P.StiffnessKernel(mesh))
     dm = DeviceMesh(mesh.q, mesh.me, mesh.vols)
@@ -126,7 +130,9 @@ def test_deterministic_run_to_run(cuda_ok):
     assert len(h) == 1
 
 
-def test_degenerate_element_named(cuda_ok):
+@pytest.mark.parametrize("kernel", ["rowgather", "twopass"])
+def test_degenerate_element_named(cuda_ok, kernel, monkeypatch):
+    monkeypatch.setenv("SA_KERNEL", kernel)
     q = np.array([[0.0, 1.0, 2.0, 0.0], [0.0, 1.0, 2.0, 1.0]])
     me = np.array([[0, 0], [3, 1], [1, 2]])
     mesh = P.Mesh(q, me, np.array([0.5, 0.0]))
@@ -171,10 +177,12 @@ def test_full_size_c2_properties(cuda_ok):
     assert np.max(np.abs(rs)) < 1e-9                    # constants are in the kernel
 
 
+@pytest.mark.parametrize("kernel", ["tile", "twopass", "rowgather"])
 @pytest.mark.parametrize("name", golden_cases())
-def test_golden_bitwise_tile_kernel(cuda_ok, name, monkeypatch):
-    # the tile kernel (templates + per-tile element dedupe) is bitwise too
-    monkeypatch.setenv("SA_KERNEL", "tile")
+def test_golden_bitwise_kernels(cuda_ok, name, kernel, monkeypatch):
+    # every numeric kernel is bitwise: the tile kernel (templates + per-tile
+    # element dedupe), the two-pass element-rows kernel, the one-pass row gather
+    monkeypatch.setenv("SA_KERNEL", kernel)
     g = load_golden(name)
     mesh = golden_mesh(g)
     k = device_kernel_for(name, g, mesh)
@@ -192,7 +200,7 @@ def test_structured_mesh_uses_few_templates(cuda_ok, monkeypatch):
     assert st["templates_ok"] == 1 and st["templates"] <= 100, st
 
 
-@pytest.mark.parametrize("kernel", ["rowgather", "tile"])
+@pytest.mark.parametrize("kernel", ["rowgather", "tile", "twopass"])
 def test_unstructured_delaunay_mesh(cuda_ok, kernel, monkeypatch):
     # random points, Delaunay triangulation: rows have (mostly) distinct templates
     monkeypatch.setenv("SA_KERNEL", kernel)
