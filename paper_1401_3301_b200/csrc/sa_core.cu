@@ -91,8 +91,10 @@ struct sa_plan {
     // of the block's element range, and the per-incidence local-row buffer
     uint4 *epos = nullptr;         // (e_hi - e_lo): slot t of (e, alpha) in inc, or ~0u
     int64_t e_lo = 0, e_hi = 0;
-    double *kbuf = nullptr;        // (n_inc * kbuf_stride) local rows in incidence order
+    double *kbuf = nullptr;        // (n_slots * stride) local rows in warp-interleaved slot order
     int64_t kbuf_elems = 0;
+    unsigned *tp_rank = nullptr;   // (n_slots) column ranks per slot (warp-interleaved like winc)
+    int64_t tp_nslots = 0;
 };
 
 // numeric-phase arguments (shared by the per-dimension translation units)
@@ -124,6 +126,7 @@ struct NumArgs {
     // doubles per incidence), the ordered fold pass reads them
     double *kbuf; int kstride;
     const uint4 *epos; int64_t e_lo, ne;
+    const unsigned *tp_rank;   // slot of incidence k of row nl: wseg[nl >> 5] + 32 k + (nl & 31)
     double mass_coef_diag, mass_coef_off;  // 2/((d+1)(d+2)(d+3)), 1/(...) as Python computes them
     double mass_wc;  // constant weight: (wsum + w) + w, the same for every (alpha, beta)
 };
@@ -694,6 +697,60 @@ __device__ __forceinline__ bool element_compute(const ElemRaw<D> &r, ElemGeo<D> 
     return degenerate;
 }
 
+// vol / (d+1): for d = 1, 3 a power-of-two divisor, so the product with its
+// exact reciprocal is the same correctly rounded value as the division
+template <int D>
+__device__ __forceinline__ double general_s1(double vol)
+{
+    if constexpr (D == 1) return SA_MUL(vol, 0.5);
+    else if constexpr (D == 3) return SA_MUL(vol, 0.25);
+    else return __ddiv_rn(vol, (double)(D + 1));
+}
+
+// General operator, all (d+1)^2 local entries of one element with the
+// subexpressions every row shares computed once (A^s G_beta, b^s + b_beta,
+// c^s + c_alpha, a0^s + a0_alpha, the volume scalings).  Each entry's
+// operations and their order are element_krow's: bitwise the same values.
+template <int D>
+__device__ __forceinline__ void general_all_rows(const NumArgs &a, const ElemGeo<D> &g, double (&K)[D + 1][D + 1])
+{
+    const double s1 = general_s1<D>(g.vol);
+    const double s2 = __ddiv_rn(g.vol, (double)((D + 1) * (D + 2)));
+    const double cd = SA_MUL(a.mass_coef_diag, g.vol), co = SA_MUL(a.mass_coef_off, g.vol);
+    double AG[D + 1][D], bb[D + 1][D], cc[D + 1][D], a0a[D + 1];
+#pragma unroll
+    for (int b = 0; b <= D; ++b) {
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            double t = SA_MUL(g.As[i][0], g.G[b][0]);
+#pragma unroll
+            for (int j = 1; j < D; ++j) t = SA_ADD(t, SA_MUL(g.As[i][j], g.G[b][j]));
+            AG[b][i] = t;
+            bb[b][i] = SA_ADD(g.bs[i], g.bv[b][i]);
+            cc[b][i] = SA_ADD(g.cs[i], g.cv[b][i]);
+        }
+        a0a[b] = SA_ADD(g.a0s, g.a0v[b]);
+    }
+#pragma unroll
+    for (int al = 0; al <= D; ++al) {
+        const double(&ga)[D] = g.G[al];
+#pragma unroll
+        for (int b = 0; b <= D; ++b) {
+            double diff = SA_MUL(ga[0], AG[b][0]);
+            double conv = SA_MUL(bb[b][0], ga[0]);
+            double tran = SA_MUL(cc[al][0], g.G[b][0]);
+#pragma unroll
+            for (int i = 1; i < D; ++i) {
+                diff = SA_ADD(diff, SA_MUL(ga[i], AG[b][i]));
+                conv = SA_ADD(conv, SA_MUL(bb[b][i], ga[i]));
+                tran = SA_ADD(tran, SA_MUL(cc[al][i], g.G[b][i]));
+            }
+            const double rea = SA_MUL(b == al ? cd : co, SA_ADD(a0a[al], g.a0v[b]));
+            K[al][b] = SA_ADD(SA_ADD(SA_SUB(SA_MUL(diff, s1), SA_MUL(conv, s2)), SA_MUL(tran, s2)), rea);
+        }
+    }
+}
+
 // K2: local row ALPHA of every requested operator, stored to dst with layout
 // dst[((b * NOUT + o) * M + l) * M + n] (entry (dof row (l, ALPHA), dof col (n, b))).
 template <int D, int M, int OPS, int ALPHA>
@@ -732,7 +789,7 @@ __device__ __forceinline__ void element_krow(const NumArgs &a, const ElemGeo<D> 
         ++o;
     }
     if constexpr ((OPS & OP_GENERAL) != 0) {
-        const double s1 = __ddiv_rn(g.vol, (double)(D + 1));
+        const double s1 = general_s1<D>(g.vol);
         const double s2 = __ddiv_rn(g.vol, (double)((D + 1) * (D + 2)));
         const double cd = SA_MUL(a.mass_coef_diag, g.vol), co = SA_MUL(a.mass_coef_off, g.vol);
         const double(&ga)[D] = g.G[ALPHA];
@@ -875,10 +932,13 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a)
         int64_t t = t0;
         if constexpr (PRE) {
             // two-pass fold: the element pass left this incidence's local
-            // row(s) at kbuf[t * kstride]; records and rows are independent
-            // loads (no dependent gather chain), ILP incidences in flight
-            auto loadk = [&](int64_t tt, double(&v)[VPR]) {
-                const double *src = a.kbuf + tt * a.kstride;
+            // row(s) in its slot (warp-interleaved: incidence k of lane j of
+            // the warp at wseg + 32 k + j, so each warp load is one contiguous
+            // run); ranks and rows are independent loads -- no gather chain,
+            // U incidences in flight
+            const int64_t sb = a.wseg[nl >> 5] + lane;
+            auto loadk = [&](int64_t slot, double(&v)[VPR]) {
+                const double *src = a.kbuf + slot * a.kstride;
                 if constexpr (VPR % 4 == 0) {
 #pragma unroll
                     for (int i = 0; i < VPR; i += 4) ldg256(src + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
@@ -900,16 +960,18 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a)
                 double v[U][VPR];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    rk[u] = __ldg(&a.inc[t + u].y);
-                    loadk(t + u, v[u]);
+                    const int64_t slot = sb + 32 * (t + u - t0);
+                    rk[u] = __ldg(a.tp_rank + slot);
+                    loadk(slot, v[u]);
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) accum(v[u], rk[u]);
             }
             for (; t < t1; ++t) {
                 double v[VPR];
-                const unsigned rk = __ldg(&a.inc[t].y);
-                loadk(t, v);
+                const int64_t slot = sb + 32 * (t - t0);
+                const unsigned rk = __ldg(a.tp_rank + slot);
+                loadk(slot, v);
                 accum(v, rk);
             }
         } else if constexpr (ILP == 3) {
@@ -1008,10 +1070,33 @@ __device__ __forceinline__ void st256(double *p, double a, double b, double c, d
     asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
 
+template <int VPR>
+__device__ __forceinline__ void store_row(double *dst, const double (&vals)[VPR])
+{
+    if constexpr (VPR % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < VPR; i += 4) st256(dst + i, vals[i], vals[i + 1], vals[i + 2], vals[i + 3]);
+    } else if constexpr (VPR % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < VPR; i += 2) *(double2 *)(dst + i) = make_double2(vals[i], vals[i + 1]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < VPR; ++i) dst[i] = vals[i];
+    }
+}
+
 template <int D, int M, int OPS, int A = 0>
 __device__ __forceinline__ void element_rows_store(const NumArgs &a, const ElemGeo<D> &g, const unsigned (&pos)[4])
 {
     constexpr int VPR = (D + 1) * n_outputs<OPS>() * M * M;
+    if constexpr (OPS == OP_GENERAL && A == 0) {
+        double K[D + 1][D + 1];
+        general_all_rows<D>(a, g, K);
+#pragma unroll
+        for (int al = 0; al <= D; ++al)
+            if (pos[al] != 0xffffffffu) store_row<D + 1>(a.kbuf + (int64_t)pos[al] * a.kstride, K[al]);
+        return;
+    }
     if (pos[A] != 0xffffffffu) {
         double vals[VPR];
         element_krow<D, M, OPS, A>(a, g, vals);
@@ -1030,20 +1115,21 @@ __device__ __forceinline__ void element_rows_store(const NumArgs &a, const ElemG
     if constexpr (A < D) element_rows_store<D, M, OPS, A + 1>(a, g, pos);
 }
 
-template <int D, int M, int OPS, int CORE>
-__global__ void __launch_bounds__(128) k_element_rows(NumArgs a)
+template <int D, int M, int OPS, int CORE, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_element_rows(NumArgs a)
 {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= a.ne) return;
+    const int64_t e = a.e_lo + i;
+    // slot map, connectivity and volume are independent: one round trip
     const uint4 p = __ldg(a.epos + i);
+    ElemRaw<D> x;
+    element_load1<D, OPS>(a, e, x);
     const unsigned pos[4] = {p.x, p.y, p.z, p.w};
     bool any = false;
 #pragma unroll
     for (int k = 0; k <= D; ++k) any |= pos[k] != 0xffffffffu;
     if (!any) return;   // element does not touch the block
-    const int64_t e = a.e_lo + i;
-    ElemRaw<D> x;
-    element_load1<D, OPS>(a, e, x);
     element_load2<D, OPS>(a, x);
     ElemGeo<D> g;
     if (element_compute<D, OPS, CORE>(x, g)) atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)e);
@@ -1070,13 +1156,22 @@ __global__ void k_inc_erange(const uint2 *__restrict__ inc, int64_t n, unsigned 
     }
 }
 
-// slot of (e, alpha): epos[e - e_lo].alpha = t
-__global__ void k_epos_fill(const uint2 *__restrict__ inc, int64_t n, unsigned e_lo, unsigned *__restrict__ epos)
+// slots of node row nl's incidences (warp-interleaved, as winc): slot map of
+// (e, alpha) and the column ranks per slot
+__global__ void k_tp_slots(const int64_t *__restrict__ inc_ptr, const uint2 *__restrict__ inc, int64_t nnodes,
+                           const int64_t *__restrict__ wseg, unsigned e_lo, unsigned *__restrict__ epos,
+                           unsigned *__restrict__ rank)
 {
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    const unsigned x = inc[t].x;
-    epos[(int64_t)((x & 0x3fffffffu) - e_lo) * 4 + (x >> 30)] = (unsigned)t;
+    const int64_t nl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (nl >= nnodes) return;
+    const int64_t base = wseg[nl >> 5] + (nl & 31);
+    const int64_t t0 = inc_ptr[nl], n = inc_ptr[nl + 1] - t0;
+    for (int64_t k = 0; k < n; ++k) {
+        const uint2 rec = inc[t0 + k];
+        const int64_t slot = base + 32 * k;
+        epos[(int64_t)((rec.x & 0x3fffffffu) - e_lo) * 4 + (rec.x >> 30)] = (unsigned)slot;
+        rank[slot] = rec.y;
+    }
 }
 
 // element lane: local row A of the element -> scatter into the fold array
@@ -1829,7 +1924,16 @@ template <int D, int M, int OPS, int CORE>
 int launch_twopass(const NumArgs &a, int64_t nnodes, cudaStream_t st)
 {
     constexpr int NOUT = n_outputs<OPS>();
-    if (a.ne) SA_LAUNCH((k_element_rows<D, M, OPS, CORE>), grid_for(a.ne, 128), 128, 0, st, a);
+    // SA_EMINB (0|3|4): minimum resident 128-thread blocks per SM of the
+    // element pass (register cap)
+    const char *emb_s = getenv("SA_EMINB");
+    // (measured on C5: no cap 210 registers 11.8 ms, 3 blocks 8.6 ms, 4 blocks 9.0 ms)
+    const int eminb = emb_s ? atoi(emb_s) : 3;
+    if (a.ne) {
+        if (eminb == 4) SA_LAUNCH((k_element_rows<D, M, OPS, CORE, 4>), grid_for(a.ne, 128), 128, 0, st, a);
+        else if (eminb == 3) SA_LAUNCH((k_element_rows<D, M, OPS, CORE, 3>), grid_for(a.ne, 128), 128, 0, st, a);
+        else SA_LAUNCH((k_element_rows<D, M, OPS, CORE, 1>), grid_for(a.ne, 128), 128, 0, st, a);
+    }
     const char *ilp_s = getenv("SA_ILP");
     const int ilp = ilp_s ? atoi(ilp_s) : 2;
     const size_t per_thread = (size_t)NOUT * (a.acc_stride | 1) * sizeof(double);
@@ -2013,7 +2117,7 @@ int sa_plan_destroy(sa_plan *P)
     if (!P) return SA_OK;
     free_all({P->inc_ptr, P->inc, P->winc, P->wseg, P->colptr, P->cols, P->indptr, P->indices, P->counters, P->scan_tmp, P->inc_e,
               P->fold, P->tile_e0, P->tile_tm, P->tm_off, P->tm, P->ck_tm, P->ck_pb, P->ck_tm_off, P->ck_tmw,
-              P->ck_flags, P->ck_rs, P->epos, P->kbuf});
+              P->ck_flags, P->ck_rs, P->epos, P->kbuf, P->tp_rank});
     delete P;
     return SA_OK;
 }
@@ -2095,7 +2199,7 @@ static bool want_twopass(int ops, int d, int m)
 
 // element range, slot map and row buffer of a plan's two-pass numeric phase
 // (built on first use, kept with the plan)
-static int ensure_twopass(sa_plan *P, int64_t kelems, cudaStream_t st)
+static int ensure_twopass(sa_plan *P, int kstride, cudaStream_t st)
 {
     if (!P->epos) {
         unsigned long long h[2] = {0xffffffffull, 0};
@@ -2111,12 +2215,28 @@ static int ensure_twopass(sa_plan *P, int64_t kelems, cudaStream_t st)
         P->e_lo = P->n_inc ? (int64_t)h[0] : 0;
         P->e_hi = P->n_inc ? (int64_t)h[1] + 1 : 0;
         const int64_t ne = P->e_hi - P->e_lo;
+        const int64_t nn = P->nnodes, nw = (nn + 31) / 32;
+        if (!P->wseg) {   // warp-interleaved slot offsets (built with winc in 3D)
+            int64_t *span = nullptr;
+            SA_CUDA_TRY(cudaMallocAsync((void **)&span, (nw + 1) * sizeof(int64_t), st));
+            SA_CUDA_TRY(cudaMallocAsync((void **)&P->wseg, (nw + 1) * sizeof(int64_t), st));
+            if (nw) SA_LAUNCH(k_warp_span, grid_for(nw, 128), 128, 0, st, P->inc_ptr, nn, span);
+            SA_TRY(exclusive_scan_i64(span, P->wseg, nw, P->scan_tmp, st));
+            SA_CUDA_TRY(cudaFreeAsync(span, st));
+        }
+        SA_CUDA_TRY(cudaMemcpyAsync(&P->tp_nslots, P->wseg + nw, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        if (P->tp_nslots >= 0xffffffffLL)
+            return set_error(SA_ERR_CAPACITY, "two-pass numeric: %lld slots overflow 32-bit slot indices",
+                             (long long)P->tp_nslots);
         SA_CUDA_TRY(cudaMallocAsync((void **)&P->epos, std::max<int64_t>(ne, 1) * sizeof(uint4), st));
         SA_CUDA_TRY(cudaMemsetAsync(P->epos, 0xff, std::max<int64_t>(ne, 1) * sizeof(uint4), st));
-        if (P->n_inc)
-            SA_LAUNCH(k_epos_fill, grid_for(P->n_inc, 256), 256, 0, st, P->inc, P->n_inc, (unsigned)P->e_lo,
-                      (unsigned *)P->epos);
+        SA_CUDA_TRY(cudaMallocAsync((void **)&P->tp_rank, std::max<int64_t>(P->tp_nslots, 1) * sizeof(unsigned), st));
+        if (nn)
+            SA_LAUNCH(k_tp_slots, grid_for(nn, 128), 128, 0, st, P->inc_ptr, P->inc, nn, P->wseg, (unsigned)P->e_lo,
+                      (unsigned *)P->epos, P->tp_rank);
     }
+    const int64_t kelems = (int64_t)kstride * P->tp_nslots;
     if (P->kbuf_elems < kelems) {
         if (P->kbuf) SA_CUDA_TRY(cudaFreeAsync(P->kbuf, st));
         P->kbuf = nullptr;
@@ -2169,12 +2289,14 @@ int sa_numeric(sa_plan *P, int ops, const sa_coeffs *cf, double *const *vals_dev
     if (want_twopass(ops, d, P->m) && P->n_inc < 0xffffffffLL) {
         const int vpr = (d + 1) * nout * P->m * P->m;
         const int ks = vpr;   // row alignment follows from the row size (see loadk)
-        SA_TRY(ensure_twopass(P, (int64_t)ks * P->n_inc, st));
+        SA_TRY(ensure_twopass(P, ks, st));
         a.kbuf = P->kbuf;
         a.kstride = ks;
         a.epos = P->epos;
         a.e_lo = P->e_lo;
         a.ne = P->e_hi - P->e_lo;
+        a.tp_rank = P->tp_rank;
+        a.wseg = P->wseg;
     }
     SA_CUDA_TRY(cudaMemsetAsync(P->counters, 0, 4 * sizeof(int64_t), st));
     SA_CUDA_TRY(cudaMemsetAsync(P->counters + 4, 0x7f, sizeof(int64_t), st));
