@@ -93,7 +93,21 @@ def _morton_renumber(q, me, n):
     return np.ascontiguousarray(q[:, perm]), np.ascontiguousarray(inv[me])
 
 
-def make_kernels(cfg, mesh):
+def general_coeffs(cfg, nq):
+    """C5 nodal fields: A = I + 0.5 R R^T / 3, b, c ~ N(0,1),
+    a0 ~ U[0,1), drawn over the global node numbering."""
+    rng = np.random.default_rng(cfg["seed"])
+    R = rng.standard_normal((nq, 3, 3))
+    A = np.eye(3)[None] + 0.5 * np.einsum("nij,nkj->nik", R, R) / 3.0
+    b = rng.standard_normal((nq, 3))
+    c = rng.standard_normal((nq, 3))
+    a0 = rng.uniform(0.0, 1.0, nq)
+    return dict(A=A, b=b, c=c, a0=a0)
+
+
+def make_kernels(cfg, mesh, window=None):
+    """Kernel descriptors of the config on ``mesh``; ``window`` maps global
+    per-node arrays to the mesh's nodes (a rank's slab)."""
     import paper_1401_3301_b200 as P
 
     out = []
@@ -105,14 +119,11 @@ def make_kernels(cfg, mesh):
         elif op == "elastic":
             out.append(P.ElasticKernel(mesh, 1.0, 0.5))
         else:
-            nq = mesh.q.shape[1]
-            rng = np.random.default_rng(cfg["seed"])
-            R = rng.standard_normal((nq, 3, 3))
-            A = np.eye(3)[None] + 0.5 * np.einsum("nij,nkj->nik", R, R) / 3.0
-            b = rng.standard_normal((nq, 3))
-            c = rng.standard_normal((nq, 3))
-            a0 = rng.uniform(0.0, 1.0, nq)
-            out.append(P.GeneralKernel(mesh, A=A, b=b, c=c, a0=a0))
+            nq = mesh.q.shape[1] if window is None else window[1]
+            f = general_coeffs(cfg, nq)
+            if window is not None:
+                f = {k: np.ascontiguousarray(v[window[0]:window[0] + mesh.q.shape[1]]) for k, v in f.items()}
+            out.append(P.GeneralKernel(mesh, **f))
     return out
 
 
@@ -241,6 +252,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = per-GPU work fixed (refined global mesh), strong = the config mesh split N ways")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -258,25 +271,47 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # SA_BENCH_SAME_GPU=1: functional check of the multi-rank logic with every
+    # rank on cuda:0 and gloo collectives (not a measurement)
+    same_gpu = os.environ.get("SA_BENCH_SAME_GPU") == "1"
+    torch.cuda.set_device(0 if same_gpu else local)
+    dev = torch.device("cuda", 0 if same_gpu else local)
+    coll_dev = torch.device("cpu") if same_gpu else dev
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
-    q, me = make_mesh(cfg)
+    # Weak scaling (default): the global mesh is refined so each rank's row
+    # block holds about one config-sized share (n_g = n * P^(1/d)); strong
+    # scaling: the config's mesh split P ways.  Each rank holds only its slab
+    # (elements touching its rows), assembled with no data-path collective.
+    d = cfg["d"]
+    n_g = cfg["n"] if (world == 1 or args.scaling == "strong") else int(round(cfg["n"] * world ** (1.0 / d)))
+    gcfg = dict(cfg, n=n_g)
+    q, me = make_mesh(gcfg)
     nq, nme = q.shape[1], me.shape[1]
-    vols = P.device_volumes(q, me)
-    mesh = P.Mesh(q, me, vols)
-    kernels = make_kernels(cfg, mesh)
-    m = kernels[0].m
+    m = d if "elastic" in cfg["ops"] else 1
     rb, re_ = parallel.row_blocks(nq, m, world)[rank]
+    if world > 1:
+        sl = parallel.slab(q, me, m, rb, re_)
+        q_r, me_r, col_off, lo = sl.q, sl.me, sl.col_offset, sl.node_lo
+        rb_r, re_r = sl.row_begin, sl.row_end
+        del q, me
+    else:
+        q_r, me_r, col_off, lo, rb_r, re_r = q, me, 0, 0, rb, re_
+    vols = P.device_volumes(q_r, me_r)
+    mesh = P.Mesh(q_r, me_r, vols)
+    kernels = make_kernels(gcfg, mesh, window=(lo, nq))
+    assert kernels[0].m == m
 
     # --- symbolic phase (once per mesh), timed separately
-    dm = D.DeviceMesh(q, me, vols)
+    dm = D.DeviceMesh(q_r, me_r, vols)
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
-    plan = dm.plan(m, rb, re_)
+    plan = dm.plan(m, rb_r, re_r)
     ev1.record()
     torch.cuda.synchronize()
     t_sym_ms = ev0.elapsed_time(ev1)
@@ -308,27 +343,28 @@ def main():
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     t_local = sum(step_ms)
-    t = torch.tensor([t_local], dtype=torch.float64, device=dev)
+    t = torch.tensor([t_local], dtype=torch.float64, device=coll_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_total_ms = float(t.item())
     ms_per_step = t_total_ms / args.steps
-    value = nme / (ms_per_step * 1e-3)
+    value = nme / (ms_per_step * 1e-3)   # global elements (each counted once) / max-over-ranks time
 
     # global nnz (all blocks) for nnz/s and the roofline's value bytes
     nnz_struct = plan.nnz
     if world > 1:
-        _off, nnz_struct_all, _ = parallel.global_offsets(plan.nnz, device=dev)
+        _off, nnz_struct_all, _ = parallel.global_offsets(plan.nnz, device=coll_dev)
     else:
         nnz_struct_all = nnz_struct
     nnz_out = [nnz_struct_all - 0 for _ in kernels]
     b_num = algorithmic_bytes(cfg, nq, nme, nnz_out)
     peak, peak_kind = load_peaks()
+    peak *= world          # aggregate over the ranks (frac stays per-GPU)
     achieved = b_num / (ms_per_step * 1e-3) / 1e9
 
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(cfg, q, me, vols, kernels, rb, re_, m, args, world, dev)
+        e2e = run_e2e(q_r, me_r, vols, kernels, rb_r, re_r, col_off, nme, args, world, coll_dev)
 
     if rank != 0:
         if world > 1:
@@ -349,11 +385,15 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": ms_per_step,
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": args.config, **config_desc(cfg), "nq": nq, "nme": nme,
+        "config": {"workload": args.config, **config_desc(gcfg), "nq": nq, "nme": nme,
+                   "per_rank": ("row block of a mesh refined to P x the config (n_g = n P^(1/d)); each rank "
+                                "holds only its slab" if args.scaling == "weak" else
+                                "row block of the config mesh; each rank holds only its slab")
+                   if world > 1 else "whole mesh",
                    "nnz_structural_per_matrix": nnz_struct_all, "n_out": len(kernels),
                    "exact_zero_entries": zeros, "parallelism": f"row-blocks x{world}",
                    "plan": {k: v for k, v in plan.stats().items()
@@ -381,11 +421,12 @@ def main():
         dist.destroy_process_group()
 
 
-def run_e2e(cfg, q, me, vols, kernels, rb, re_, m, args, world, dev):
+def run_e2e(q, me, vols, kernels, rb, re_, col_offset, nme_global, args, world, dev):
     """Same metric through the public API with host buffers: every step calls
-    assemble_block_b200 on a Mesh whose q/me/vols live in pinned host memory:
-    upload, symbolic phase, numeric phase, exact-zero compaction, download of
-    the canonical CSR (int64 indices, f64 values) into pinned host memory."""
+    assemble_block_b200 on a Mesh whose q/me/vols live in pinned host memory
+    (the rank's slab at N > 1): upload, symbolic phase, numeric phase,
+    exact-zero compaction, download of the canonical CSR (int64 global column
+    indices, f64 values) into pinned host memory."""
     import torch
 
     import paper_1401_3301_b200 as P
@@ -403,7 +444,8 @@ def run_e2e(cfg, q, me, vols, kernels, rb, re_, m, args, world, dev):
     for i in range(steps + 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        blocks = assemble_block_b200(mesh, kernels, rb, re_, timings=stages if i > 0 else None)
+        blocks = assemble_block_b200(mesh, kernels, rb, re_, timings=stages if i > 0 else None,
+                                     col_offset=col_offset)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         if i > 0:
@@ -420,8 +462,7 @@ def run_e2e(cfg, q, me, vols, kernels, rb, re_, m, args, world, dev):
         import torch.distributed as dist
 
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    nme = me.shape[1]
-    return {"value": nme / float(t.item()), "unit": "elements/s", "h2d_bytes_per_step": int(h2d),
+    return {"value": nme_global / float(t.item()), "unit": "elements/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": float(t.item()) * 1e3,
             "stages_ms": {k: v / steps for k, v in stages.items()},
             "path": "assemble_block_b200(Mesh(pinned q, me, vols)): upload -> symbolic -> numeric -> compact -> "

@@ -78,10 +78,11 @@ def to_host(csr: DeviceCSR, nrows_total: int | None = None) -> SparseMatrix:
     return SparseMatrix(nrows, csr.ncols, row_ptr, col_idx, vals)
 
 
-def to_host_many(csrs, nrows_total=None) -> list[SparseMatrix]:
+def to_host_many(csrs, nrows_total=None, col_offset: int = 0) -> list[SparseMatrix]:
     """Download several results; fused outputs that share one pattern (no
     exact-zero entries dropped) share the host row_ptr/col_idx arrays, so the
-    pattern crosses PCIe once."""
+    pattern crosses PCIe once.  ``col_offset`` is added to the column indices
+    on the device (a slab's local columns -> global dofs)."""
     import torch
 
     cache = {}
@@ -89,7 +90,10 @@ def to_host_many(csrs, nrows_total=None) -> list[SparseMatrix]:
     for c in csrs:
         key = (c.indptr.data_ptr(), c.indices.data_ptr(), c.indices.numel())
         if key not in cache:
-            srcs = (c.indptr, c.indices.to(torch.int64))
+            ix = c.indices.to(torch.int64)
+            if col_offset:
+                ix += col_offset
+            srcs = (c.indptr, ix)
             pinned = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in srcs]
             for o, t in zip(pinned, srcs):
                 o.copy_(t, non_blocking=True)
@@ -123,11 +127,13 @@ def assemble_many_b200(mesh, kernels, core: str = "SkylakeX", cache: bool = True
 
 
 def assemble_block_b200(mesh, kernels, row_begin: int, row_end: int, core: str = "SkylakeX",
-                        timings: dict | None = None):
+                        timings: dict | None = None, col_offset: int = 0):
     """Rows [row_begin, row_end) of the fused assembly, end to end from host
     arrays (the per-rank call of the row-block data-parallel path): upload,
     symbolic, numeric, exact-zero compaction, download.  Returns one
-    (indptr, indices, vals) host block per kernel."""
+    (indptr, indices, vals) host block per kernel.  For a rank's slab
+    (parallel.slab) pass its local rows and ``col_offset`` to get global
+    column dofs."""
     import time
 
     import torch
@@ -142,7 +148,7 @@ def assemble_block_b200(mesh, kernels, row_begin: int, row_end: int, core: str =
     csrs = plan.assemble(kernels)
     torch.cuda.current_stream().synchronize()
     t3 = time.perf_counter()
-    out = to_host_many(csrs)
+    out = to_host_many(csrs, col_offset=col_offset)
     t4 = time.perf_counter()
     dm.close()
     if timings is not None:

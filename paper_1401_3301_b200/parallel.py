@@ -11,6 +11,8 @@ torch.distributed (NCCL on the B200 box, gloo in the CPU tests).
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
 
 
@@ -21,6 +23,49 @@ def row_blocks(nq: int, m: int, nparts: int) -> list[tuple[int, int]]:
         raise ValueError("nparts must be >= 1")
     cuts = [(nq * p) // nparts for p in range(nparts + 1)]
     return [(m * cuts[p], m * cuts[p + 1]) for p in range(nparts)]
+
+
+@dataclass
+class Slab:
+    """The part of a mesh one rank needs for its row block: the elements
+    touching the block's nodes, in their original (ascending) order, over the
+    window [node_lo, node_lo + nq_local) of nodes they reference, renumbered
+    from 0.  Rows [row_begin, row_end) of the local problem are the block's
+    rows; local column dof c is global column dof c + col_offset.  Because
+    the element order is kept, the block assembled from the slab is bitwise
+    the block of the full mesh (same contributions, same fold order)."""
+
+    q: np.ndarray          # (d, nq_local) f64
+    me: np.ndarray         # (d+1, nme_local) int64, local node ids
+    vols: np.ndarray | None
+    node_lo: int
+    row_begin: int         # local dof rows of the block
+    row_end: int
+    col_offset: int        # m * node_lo
+    elements: np.ndarray   # global ids of the slab's elements (ascending)
+
+    def nodal(self, a):
+        """Window of a per-node array (nq, ...) or None."""
+        return None if a is None else np.ascontiguousarray(np.asarray(a)[self.node_lo:self.node_lo + self.q.shape[1]])
+
+
+def slab(q, me, m: int, row_begin: int, row_end: int, vols=None) -> Slab:
+    """Slab of dof rows [row_begin, row_end) (node aligned) of mesh (q, me)."""
+    if row_begin % m or row_end % m:
+        raise ValueError("row block must be node aligned")
+    nb0, nb1 = row_begin // m, row_end // m
+    me = np.asarray(me)
+    touch = np.zeros(me.shape[1], dtype=bool)
+    for a in range(me.shape[0]):
+        touch |= (me[a] >= nb0) & (me[a] < nb1)
+    sel = np.flatnonzero(touch)
+    mes = me[:, sel]
+    lo, hi = nb0, nb1
+    if sel.size:
+        lo, hi = min(lo, int(mes.min())), max(hi, int(mes.max()) + 1)
+    return Slab(q=np.ascontiguousarray(np.asarray(q)[:, lo:hi]), me=np.ascontiguousarray(mes - lo),
+                vols=None if vols is None else np.ascontiguousarray(np.asarray(vols)[sel]),
+                node_lo=lo, row_begin=m * (nb0 - lo), row_end=m * (nb1 - lo), col_offset=m * lo, elements=sel)
 
 
 def global_offsets(local_nnz: int, group=None, device=None) -> tuple[int, int, list[int]]:

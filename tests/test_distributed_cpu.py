@@ -24,7 +24,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, name, result_q):
+def _worker(rank, world, port, name, result_q, use_slab=False):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -43,7 +43,18 @@ def _worker(rank, world, port, name, result_q):
         op = oo(name, g)
         nq = g["q"].shape[1]
         rb, re_ = parallel.row_blocks(nq, op.m, world)[rank]
-        ip, ix, va = O.assemble_block(g["q"], g["me"], op, rb, re_)
+        if use_slab:
+            # the rank only holds its slab: elements touching its rows, local
+            # node numbering; columns shifted back to global dofs
+            sl = parallel.slab(g["q"], g["me"], op.m, rb, re_, g["vols"])
+            gl = dict(g, q=sl.q, me=sl.me, vols=sl.vols)
+            for key in ("w", "lamb", "mu", "A", "b", "c", "a0"):
+                if key in g:
+                    gl[key] = sl.nodal(g[key])
+            ip, ix, va = O.assemble_block(sl.q, sl.me, oo(name, gl), sl.row_begin, sl.row_end)
+            ix = ix + sl.col_offset
+        else:
+            ip, ix, va = O.assemble_block(g["q"], g["me"], op, rb, re_)
         off, total, counts = parallel.global_offsets(len(va))
         blocks = parallel.gather_blocks_to_root((rb, re_, ip, ix, va))
         if rank == 0:
@@ -57,12 +68,13 @@ def _worker(rank, world, port, name, result_q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("use_slab", [False, True])
 @pytest.mark.parametrize("name", ["stiff_d3_n6_jit", "elastic_d2_n15_jit", "general_d2_n15_jit"])
-def test_two_rank_row_blocks_stitch_to_full_matrix(name):
+def test_two_rank_row_blocks_stitch_to_full_matrix(name, use_slab):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, q, use_slab)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:

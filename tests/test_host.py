@@ -120,3 +120,27 @@ def test_register_into_reference_registries():
         assert "b200" in rb.VARIANTS_FOR["stiffness"] and "b200" in rb.VARIANTS_FOR["elastic"]
     finally:
         sys.path.remove(ref)
+
+
+def test_slabs_reproduce_full_rows_bitwise():
+    # P row blocks assembled from their slabs (elements touching the block,
+    # local node window) stitch to the full optv2 matrix, bitwise
+    import paper_1401_3301_b200 as P
+    from oracle import oracle as O
+    from paper_1401_3301_b200 import parallel
+
+    for d, n, parts in ((2, 24, 3), (3, 7, 4)):
+        q, me = P.hypercube_arrays(d, n)
+        q = P.jitter_interior(q, n, 0.2 if d == 2 else 0.15, 11)
+        vols = O.volumes(q, me)
+        nq = q.shape[1]
+        rp, ci, va = O.assemble_block(q, me, O.OracleOp("stiffness", d, vols))
+        blocks = []
+        for rb, re_ in parallel.row_blocks(nq, 1, parts):
+            sl = parallel.slab(q, me, 1, rb, re_, vols)
+            assert sl.me.shape[1] < me.shape[1]
+            ip, ix, vv = O.assemble_block(sl.q, sl.me, O.OracleOp("stiffness", d, sl.vols), sl.row_begin,
+                                          sl.row_end)
+            blocks.append((rb, re_, ip, ix + sl.col_offset, vv))
+        r2, c2, v2 = parallel.stitch(blocks, nq, nq)
+        assert np.array_equal(r2, rp) and np.array_equal(c2, ci) and np.array_equal(v2, va)
