@@ -12,6 +12,7 @@
 // and the value-dependent pattern (sparse.py:108-111) follows exactly.
 // No atomics touch values: the output is deterministic by construction.
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 #include <unordered_map>
@@ -95,6 +96,12 @@ struct sa_plan {
     int64_t kbuf_elems = 0;
     unsigned *tp_rank = nullptr;   // (n_slots) column ranks per slot (warp-interleaved like winc)
     int64_t tp_nslots = 0;
+    // element batches (two-pass element pass, 3D general operator): per batch
+    // of EB_SIZE consecutive elements its sorted unique vertices (EB_CAP max;
+    // count -1 = too many, direct gathers) and 8-bit local vertex ids per element
+    int32_t *eb_verts = nullptr, *eb_count = nullptr;
+    uint32_t *eb_loc = nullptr;
+    int eb_maxn = 0;
 };
 
 // numeric-phase arguments (shared by the per-dimension translation units)
@@ -127,6 +134,9 @@ struct NumArgs {
     double *kbuf; int kstride;
     const uint4 *epos; int64_t e_lo, ne;
     const unsigned *tp_rank;   // slot of incidence k of row nl: wseg[nl >> 5] + 32 k + (nl & 31)
+    const int32_t *eb_verts, *eb_count;
+    const uint32_t *eb_loc;
+    int eb_maxn;
     double mass_coef_diag, mass_coef_off;  // 2/((d+1)(d+2)(d+3)), 1/(...) as Python computes them
     double mass_wc;  // constant weight: (wsum + w) + w, the same for every (alpha, beta)
 };
@@ -1136,6 +1146,177 @@ __global__ void __launch_bounds__(128, MINB) k_element_rows(NumArgs a)
     element_rows_store<D, M, OPS>(a, g, pos);
 }
 
+// ---------------------------------------------------------------------------
+// Batched element pass: a block takes EB_SIZE consecutive elements, stages
+// the batch's distinct vertices (coordinates + packed nodal coefficients,
+// EB_REC doubles each) ONCE in shared memory with cp.async, then every
+// thread computes its element from the stage.  A vertex is shared by ~24
+// tetrahedra, so a batch of 128 consecutive elements of a Kuhn mesh needs
+// ~90 records instead of 512 register gathers; the compute phase holds no
+// load destinations, so more warps fit and the fp64 pipe stays fed.
+constexpr int EB_SIZE = 128;   // elements per batch
+constexpr int EB_CAP = 255;    // distinct vertices per batch (8-bit local ids)
+constexpr int EB_REC = 20;     // staged doubles per vertex: q (4, padded) + [A(9) b(3) c(3) a0]
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// symbolic (once per plan): sorted unique vertices of every batch, local ids
+template <int D>
+__global__ void __launch_bounds__(EB_SIZE) k_eb_build(const typename IdxT<D>::type *__restrict__ me, int64_t e_lo,
+                                                      int64_t ne, int32_t *__restrict__ verts,
+                                                      int32_t *__restrict__ count, uint32_t *__restrict__ loc,
+                                                      unsigned long long *maxn)
+{
+    constexpr int NK = 4 * EB_SIZE;
+    __shared__ int keys[NK];
+    __shared__ int part[EB_SIZE / 32];
+    __shared__ int nuniq;
+    const int t = threadIdx.x;
+    const int64_t b = blockIdx.x, i = b * EB_SIZE + t;
+    int v[D + 1];
+    if (i < ne) load_element<D>(me, e_lo + i, v);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) keys[k * EB_SIZE + t] = (i < ne && k <= D) ? v[k < D + 1 ? k : 0] : INT_MAX;
+    __syncthreads();
+    // bitonic sort, NK/2 compare pairs per stage
+    for (int kk = 2; kk <= NK; kk <<= 1)
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            for (int pi = t; pi < NK / 2; pi += EB_SIZE) {
+                const int lo = 2 * j * (pi / j) + (pi % j), hi = lo + j;
+                const bool up = (lo & kk) == 0;
+                const int x = keys[lo], y = keys[hi];
+                if ((x > y) == up) { keys[lo] = y; keys[hi] = x; }
+            }
+            __syncthreads();
+        }
+    // unique: heads among this thread's 4 consecutive keys, block scan
+    int h[4], cnt = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int j = 4 * t + k;
+        h[k] = keys[j] != INT_MAX && (j == 0 || keys[j] != keys[j - 1]);
+        cnt += h[k];
+    }
+    int incl = cnt;
+#pragma unroll
+    for (int sh = 1; sh < 32; sh <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, sh);
+        if ((t & 31) >= sh) incl += y;
+    }
+    if ((t & 31) == 31) part[t >> 5] = incl;
+    __syncthreads();
+    int off = incl - cnt;
+    for (int w = 0; w < (t >> 5); ++w) off += part[w];
+    if (t == EB_SIZE - 1) nuniq = off + cnt;
+    int u[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { u[k] = off; off += h[k]; }
+    int kv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) kv[k] = keys[4 * t + k];
+    __syncthreads();
+    const int n = nuniq;
+    // compact the unique keys to the front of keys[] and to the batch list
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (h[k]) {
+            keys[u[k]] = kv[k];
+            if (n <= EB_CAP) verts[b * EB_CAP + u[k]] = kv[k];
+        }
+    __syncthreads();
+    if (t == 0) {
+        count[b] = n <= EB_CAP ? n : -1;
+        if (n <= EB_CAP) atomicMax(maxn, (unsigned long long)n);
+    }
+    if (i < ne && n <= EB_CAP) {
+        unsigned l = 0;
+#pragma unroll
+        for (int k = 0; k <= D; ++k) {
+            int lo = 0, hi = n;
+            while (lo < hi) { const int mid = (lo + hi) >> 1; if (keys[mid] < v[k]) lo = mid + 1; else hi = mid; }
+            l |= (unsigned)lo << (8 * k);
+        }
+        loc[i] = l;
+    }
+}
+
+// ElemRaw from the staged vertex records (same summation order as
+// element_load_coeffs: vertex 0..d, packed general coefficients)
+template <int D, int OPS>
+__device__ __forceinline__ void element_from_stage(const double *__restrict__ vrec, unsigned lc, ElemRaw<D> &r)
+{
+#pragma unroll
+    for (int k = 0; k <= D; ++k) {
+        const double *rec = vrec + ((lc >> (8 * k)) & 0xff) * EB_REC;
+#pragma unroll
+        for (int c = 0; c < D; ++c) r.x[k][c] = rec[c];
+        const double *w = rec + 4;
+#pragma unroll
+        for (int ii = 0; ii < D; ++ii) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) r.As[ii][j] = k == 0 ? w[ii * 3 + j] : SA_ADD(r.As[ii][j], w[ii * 3 + j]);
+            r.bv[k][ii] = w[9 + ii];
+            r.cv[k][ii] = w[12 + ii];
+            r.bs[ii] = k == 0 ? w[9 + ii] : SA_ADD(r.bs[ii], w[9 + ii]);
+            r.cs[ii] = k == 0 ? w[12 + ii] : SA_ADD(r.cs[ii], w[12 + ii]);
+        }
+        r.a0v[k] = w[15];
+        r.a0s = k == 0 ? w[15] : SA_ADD(r.a0s, w[15]);
+    }
+}
+
+template <int D, int M, int OPS, int CORE>
+__global__ void __launch_bounds__(EB_SIZE, 4) k_element_rows_batched(NumArgs a)
+{
+    extern __shared__ double vrec[];
+    const int t = threadIdx.x;
+    const int64_t b = blockIdx.x, i = b * EB_SIZE + t;
+    const bool in = i < a.ne;
+    const int64_t e = a.e_lo + i;
+    const int n = __ldg(a.eb_count + b);
+    uint4 p = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+    unsigned lc = 0;
+    ElemRaw<D> x;
+    if (in) {
+        p = __ldg(a.epos + i);
+        x.vol = __ldg(a.vols + e);
+        if (n >= 0) lc = __ldg(a.eb_loc + i);
+        else load_element<D>((const typename IdxT<D>::type *)a.me, e, x.v);
+    }
+    if (n >= 0) {   // uniform per block
+        // the batch's vertex list first (one coalesced load), then every
+        // cp.async of the stage issues without a dependent load
+        __shared__ int sv[EB_CAP + 1];
+        const int32_t *vl = a.eb_verts + b * EB_CAP;
+        for (int s = t; s < n; s += EB_SIZE) sv[s] = __ldg(vl + s);
+        __syncthreads();
+        for (int c = t; c < n * 10; c += EB_SIZE) {
+            const int s = c / 10, h = c - 10 * s;
+            const int64_t vv = sv[s];
+            const double *src = h < 2 ? (const double *)a.qv + vv * 4 + 2 * h : a.gen_packed + vv * 16 + 2 * (h - 2);
+            cp_async16(vrec + s * EB_REC + 2 * h, src);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+    }
+    if (!in) return;
+    const unsigned pos[4] = {p.x, p.y, p.z, p.w};
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k <= D; ++k) any |= pos[k] != 0xffffffffu;
+    if (!any) return;
+    if (n >= 0) element_from_stage<D, OPS>(vrec, lc, x);
+    else element_load2<D, OPS>(a, x);
+    ElemGeo<D> g;
+    if (element_compute<D, OPS, CORE>(x, g)) atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)e);
+    element_rows_store<D, M, OPS>(a, g, pos);
+}
+
 // element range of the block's incidences: out[0] = min e, out[1] = max e
 __global__ void k_inc_erange(const uint2 *__restrict__ inc, int64_t n, unsigned long long *out)
 {
@@ -1929,7 +2110,19 @@ int launch_twopass(const NumArgs &a, int64_t nnodes, cudaStream_t st)
     const char *emb_s = getenv("SA_EMINB");
     // (measured on C5: no cap 210 registers 11.8 ms, 3 blocks 8.6 ms, 4 blocks 9.0 ms)
     const int eminb = emb_s ? atoi(emb_s) : 3;
-    if (a.ne) {
+    bool batched = false;
+    if constexpr (OPS == OP_GENERAL && D == 3) {
+        if (a.eb_loc && a.gen_packed) {
+            // batched element pass (vertex records deduplicated per batch in smem)
+            batched = true;
+            const size_t smem = (size_t)std::max(a.eb_maxn, 1) * EB_REC * sizeof(double);
+            auto kern = k_element_rows_batched<D, M, OPS, CORE>;
+            SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            if (a.ne) SA_LAUNCH(kern, grid_for(a.ne, EB_SIZE), EB_SIZE, smem, st, a);
+        }
+    }
+    if (batched) {
+    } else if (a.ne) {
         if (eminb == 4) SA_LAUNCH((k_element_rows<D, M, OPS, CORE, 4>), grid_for(a.ne, 128), 128, 0, st, a);
         else if (eminb == 3) SA_LAUNCH((k_element_rows<D, M, OPS, CORE, 3>), grid_for(a.ne, 128), 128, 0, st, a);
         else SA_LAUNCH((k_element_rows<D, M, OPS, CORE, 1>), grid_for(a.ne, 128), 128, 0, st, a);
@@ -2117,7 +2310,8 @@ int sa_plan_destroy(sa_plan *P)
     if (!P) return SA_OK;
     free_all({P->inc_ptr, P->inc, P->winc, P->wseg, P->colptr, P->cols, P->indptr, P->indices, P->counters, P->scan_tmp, P->inc_e,
               P->fold, P->tile_e0, P->tile_tm, P->tm_off, P->tm, P->ck_tm, P->ck_pb, P->ck_tm_off, P->ck_tmw,
-              P->ck_flags, P->ck_rs, P->epos, P->kbuf, P->tp_rank});
+              P->ck_flags, P->ck_rs, P->epos, P->kbuf, P->tp_rank, P->eb_verts,
+              P->eb_count, P->eb_loc});
     delete P;
     return SA_OK;
 }
@@ -2199,7 +2393,7 @@ static bool want_twopass(int ops, int d, int m)
 
 // element range, slot map and row buffer of a plan's two-pass numeric phase
 // (built on first use, kept with the plan)
-static int ensure_twopass(sa_plan *P, int kstride, cudaStream_t st)
+static int ensure_twopass(sa_plan *P, int kstride, bool batches, cudaStream_t st)
 {
     if (!P->epos) {
         unsigned long long h[2] = {0xffffffffull, 0};
@@ -2235,6 +2429,23 @@ static int ensure_twopass(sa_plan *P, int kstride, cudaStream_t st)
         if (nn)
             SA_LAUNCH(k_tp_slots, grid_for(nn, 128), 128, 0, st, P->inc_ptr, P->inc, nn, P->wseg, (unsigned)P->e_lo,
                       (unsigned *)P->epos, P->tp_rank);
+    }
+    if (batches && !P->eb_loc && P->mesh->d == 3) {
+        const int64_t ne = P->e_hi - P->e_lo, nb = (ne + EB_SIZE - 1) / EB_SIZE;
+        unsigned long long *mx = nullptr;
+        SA_CUDA_TRY(cudaMallocAsync((void **)&P->eb_verts, std::max<int64_t>(nb * EB_CAP, 1) * sizeof(int32_t), st));
+        SA_CUDA_TRY(cudaMallocAsync((void **)&P->eb_count, std::max<int64_t>(nb, 1) * sizeof(int32_t), st));
+        SA_CUDA_TRY(cudaMallocAsync((void **)&P->eb_loc, std::max<int64_t>(ne, 1) * sizeof(uint32_t), st));
+        SA_CUDA_TRY(cudaMallocAsync((void **)&mx, sizeof(unsigned long long), st));
+        SA_CUDA_TRY(cudaMemsetAsync(mx, 0, sizeof(unsigned long long), st));
+        if (nb)
+            SA_LAUNCH(k_eb_build<3>, (unsigned)nb, EB_SIZE, 0, st, (const int4 *)P->mesh->me, P->e_lo, ne, P->eb_verts,
+                      P->eb_count, P->eb_loc, mx);
+        unsigned long long h = 0;
+        SA_CUDA_TRY(cudaMemcpyAsync(&h, mx, sizeof h, cudaMemcpyDeviceToHost, st));
+        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        SA_CUDA_TRY(cudaFreeAsync(mx, st));
+        P->eb_maxn = (int)h;
     }
     const int64_t kelems = (int64_t)kstride * P->tp_nslots;
     if (P->kbuf_elems < kelems) {
@@ -2289,7 +2500,15 @@ int sa_numeric(sa_plan *P, int ops, const sa_coeffs *cf, double *const *vals_dev
     if (want_twopass(ops, d, P->m) && P->n_inc < 0xffffffffLL) {
         const int vpr = (d + 1) * nout * P->m * P->m;
         const int ks = vpr;   // row alignment follows from the row size (see loadk)
-        SA_TRY(ensure_twopass(P, ks, st));
+        const char *eb_s = getenv("SA_EBATCH");
+        const bool batches = ops == SA_OP_GENERAL && d == 3 && (eb_s ? atoi(eb_s) != 0 : true);
+        SA_TRY(ensure_twopass(P, ks, batches, st));
+        if (batches) {
+            a.eb_verts = P->eb_verts;
+            a.eb_count = P->eb_count;
+            a.eb_loc = P->eb_loc;
+            a.eb_maxn = P->eb_maxn;
+        }
         a.kbuf = P->kbuf;
         a.kstride = ks;
         a.epos = P->epos;
