@@ -50,22 +50,25 @@ def load_peaks():
 
 
 def profiled_traffic(name):
-    """DRAM bytes (read + write) per launch of the numeric kernel for this
-    config, from the newest committed ncu --set full summary
-    (profiles/rNN/ncu_<config>_*.json, written by tools/ncu_summary.py);
-    null when no capture exists for the default kernel."""
+    """DRAM bytes (read + write) of one numeric step of this config (every
+    kernel of the phase), from the newest committed ncu --set full summary
+    (profiles/rNN/ncu_<config>_numeric_*.json, tools/prof_cfg.sh +
+    tools/ncu_combine.py); null when no capture exists for the default
+    kernels."""
     import glob
 
     if os.environ.get("SA_KERNEL") or os.environ.get("SA_BENCH_RENUMBER"):
         return {"traffic": None}
-    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"ncu_{name}_*.json")))
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"ncu_{name}_numeric_*.json")),
+                   key=os.path.getmtime)
     if not paths:
         return {"traffic": None}
     try:
         with open(paths[-1]) as f:
             d = json.load(f)
         return {"traffic": float(d["dram_bytes"]), "traffic_source": os.path.relpath(paths[-1], ROOT),
-                "traffic_kernel_ms": float(d["duration_ns"]) * 1e-6}
+                "traffic_kernel_ms": float(d["duration_ns"]) * 1e-6,
+                "traffic_kernels": [k["kernel"].split("(")[0].replace("void ", "") for k in d["kernels"]]}
     except Exception:
         return {"traffic": None}
 
@@ -125,6 +128,19 @@ def make_kernels(cfg, mesh, window=None):
                 f = {k: np.ascontiguousarray(v[window[0]:window[0] + mesh.q.shape[1]]) for k, v in f.items()}
             out.append(P.GeneralKernel(mesh, **f))
     return out
+
+
+def numeric_kernels(cfg):
+    """The kernel(s) of one numeric step (the default selection in
+    sa_core.cu: two-pass for the 3D general operator, row gather otherwise)."""
+    k = os.environ.get("SA_KERNEL", "")
+    if k == "tile":
+        return "k_numeric_tiles"
+    if k == "chunk":
+        return "k_numeric_chunks"
+    if k == "twopass" or (not k and cfg["d"] == 3 and cfg["ops"] == ("general",)):
+        return "k_element_rows_batched + k_numeric_rowgather<PRE> (two-pass; time = both)"
+    return "k_numeric_rowgather"
 
 
 def algorithmic_bytes(cfg, nq, nme, nnz_per_out):
@@ -406,8 +422,7 @@ def main():
         "numeric_ms": ms_per_step,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, **profiled_traffic(args.config), "peak_kind": peak_kind,
-                     "algorithmic_bytes": b_num, "kernel": {"chunk": "k_numeric_chunks", "tile": "k_numeric_tiles"}.get(
-                         os.environ.get("SA_KERNEL", ""), "k_numeric_rowgather"),
+                     "algorithmic_bytes": b_num, "kernel": numeric_kernels(cfg),
                      "frac_of_8TBps_nominal": achieved / 8000.0},
         "gpu_launches": launches,
         "clocks": clk.summary(),

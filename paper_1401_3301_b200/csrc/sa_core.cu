@@ -313,6 +313,85 @@ __global__ void k_inc_ranks(const typename IdxT<D>::type *__restrict__ me, const
     }
 }
 
+// Fused node pass of the symbolic phase (fast path, every node with at most
+// NS_CAPI incidences and NS_CAPC distinct neighbours): one thread per node
+// row, its incidences and its sorted neighbour list in private shared-memory
+// columns ([k][thread]: conflict-free).  FILL = false: sort the incidences in
+// ascending element order (written back) and count the neighbours;
+// FILL = true: (incidences already sorted) write the neighbours and the
+// 8-bit column ranks of every incidence.  Replaces k_inc_sort + 2 x
+// k_node_cols + k_inc_ranks (global-memory insertion sort, local-memory
+// neighbour buffers).
+constexpr int NS_THREADS = 64;
+constexpr int NS_CAPI = 48;
+constexpr int NS_CAPC = 64;
+
+template <int D, bool FILL>
+__global__ void __launch_bounds__(NS_THREADS) k_node_symbolic(const typename IdxT<D>::type *__restrict__ me,
+                                                              const int64_t *__restrict__ inc_ptr,
+                                                              uint2 *__restrict__ inc, int64_t nnodes,
+                                                              int64_t *__restrict__ ncol,
+                                                              const int64_t *__restrict__ colptr,
+                                                              int32_t *__restrict__ cols,
+                                                              unsigned long long *overflow)
+{
+    __shared__ unsigned s_inc[NS_CAPI][NS_THREADS];
+    __shared__ int s_col[NS_CAPC][NS_THREADS];
+    const int tid = threadIdx.x;
+    const int64_t nl = blockIdx.x * (int64_t)NS_THREADS + tid;
+    if (nl >= nnodes) return;
+    const int64_t t0 = inc_ptr[nl];
+    const int n = (int)(inc_ptr[nl + 1] - t0);
+    if (n > NS_CAPI) { atomicOr(overflow, 1ull); return; }
+    if (!FILL) {
+        for (int k = 0; k < n; ++k) {
+            const unsigned x = inc[t0 + k].x;
+            const unsigned key = x & 0x3fffffffu;
+            int u = k - 1;
+            while (u >= 0 && (s_inc[u][tid] & 0x3fffffffu) > key) { s_inc[u + 1][tid] = s_inc[u][tid]; --u; }
+            s_inc[u + 1][tid] = x;
+        }
+    } else {
+        for (int k = 0; k < n; ++k) s_inc[k][tid] = inc[t0 + k].x;
+    }
+    int nc = 0;
+    for (int k = 0; k < n; ++k) {
+        int v[D + 1];
+        load_element<D>(me, s_inc[k][tid] & 0x3fffffffu, v);
+#pragma unroll
+        for (int a = 0; a <= D; ++a) {
+            const int x = v[a];
+            int lo = 0, hi = nc;
+            while (lo < hi) { const int mid = (lo + hi) >> 1; if (s_col[mid][tid] < x) lo = mid + 1; else hi = mid; }
+            if (lo < nc && s_col[lo][tid] == x) continue;
+            if (nc == NS_CAPC) { atomicOr(overflow, 1ull); return; }
+            for (int u = nc; u > lo; --u) s_col[u][tid] = s_col[u - 1][tid];
+            s_col[lo][tid] = x;
+            ++nc;
+        }
+    }
+    if (!FILL) {
+        for (int k = 0; k < n; ++k) inc[t0 + k] = make_uint2(s_inc[k][tid], 0u);
+        ncol[nl] = nc;
+        return;
+    }
+    const int64_t c0 = colptr[nl];
+    for (int u = 0; u < nc; ++u) cols[c0 + u] = s_col[u][tid];
+    for (int k = 0; k < n; ++k) {
+        const unsigned x = s_inc[k][tid];
+        int v[D + 1];
+        load_element<D>(me, x & 0x3fffffffu, v);
+        unsigned ranks = 0;
+#pragma unroll
+        for (int a = 0; a <= D; ++a) {
+            int lo = 0, hi = nc;
+            while (lo < hi) { const int mid = (lo + hi) >> 1; if (s_col[mid][tid] < v[a]) lo = mid + 1; else hi = mid; }
+            ranks |= (unsigned)lo << (8 * a);
+        }
+        inc[t0 + k] = make_uint2(x, ranks);
+    }
+}
+
 // records per warp of 32 node rows: 32 x the warp's largest incidence count
 __global__ void k_warp_span(const int64_t *__restrict__ inc_ptr, int64_t nnodes, int64_t *__restrict__ span)
 {
@@ -1911,7 +1990,29 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
     if (M->nme)
         SA_LAUNCH(k_inc_fill<D>, ge, B, 0, st, (const I *)M->me, M->nme, P->node_begin, P->node_end, P->inc_ptr,
                   (unsigned long long *)cnt, P->inc);
-    if (nn) {
+    // fast path when every node fits the fused shared-memory node pass
+    // (max incidences <= NS_CAPI, checked here; neighbours <= NS_CAPC,
+    // checked by the pass itself), else the general kernels
+    bool fast = false;
+    const char *ns_s = getenv("SA_SYMFAST");
+    if (nn && (ns_s ? atoi(ns_s) != 0 : true)) {
+        SA_CUDA_TRY(cudaMemsetAsync(P->counters + 6, 0, 2 * sizeof(int64_t), st));
+        SA_LAUNCH(k_max_diff, std::min<int64_t>(grid_for(nn, 256), 148 * 8), 256, 0, st, P->inc_ptr, nn,
+                  (unsigned long long *)(P->counters + 6));
+        int64_t mi = 0;
+        SA_CUDA_TRY(cudaMemcpyAsync(&mi, P->counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        if (mi <= NS_CAPI) {
+            SA_LAUNCH((k_node_symbolic<D, false>), grid_for(nn, NS_THREADS), NS_THREADS, 0, st, (const I *)M->me,
+                      P->inc_ptr, P->inc, nn, cnt, (const int64_t *)nullptr, (int32_t *)nullptr,
+                      (unsigned long long *)(P->counters + 7));
+            int64_t ov = 0;
+            SA_CUDA_TRY(cudaMemcpyAsync(&ov, P->counters + 7, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            SA_CUDA_TRY(cudaStreamSynchronize(st));
+            fast = ov == 0;   // else (a node with > NS_CAPC neighbours): the general kernels below
+        }
+    }
+    if (nn && !fast) {
         SA_LAUNCH(k_inc_sort, grid_for(nn, 128), 128, 0, st, P->inc_ptr, nn, P->inc);
         SA_CUDA_TRY(cudaMemsetAsync(P->counters + 5, 0, sizeof(int64_t), st));
         SA_LAUNCH(k_node_cols<D>, grid_for(nn, 128), 128, 0, st, (const I *)M->me, P->inc_ptr, P->inc, nn, cnt,
@@ -1920,11 +2021,15 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
     SA_TRY(exclusive_scan_i64(cnt, P->colptr, nn, P->scan_tmp, st));
     int64_t cap = 0;
     SA_CUDA_TRY(cudaMemcpyAsync(&P->n_colnodes, P->colptr + nn, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SA_CUDA_TRY(cudaMemcpyAsync(&cap, P->counters + 5, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    if (!fast) SA_CUDA_TRY(cudaMemcpyAsync(&cap, P->counters + 5, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     SA_CUDA_TRY(cudaStreamSynchronize(st));
     if (cap) return set_error(SA_ERR_CAPACITY, "a node has more than %d distinct neighbours", MAXC);
     SA_CUDA_TRY(cudaMallocAsync((void **)&P->cols, std::max<int64_t>(P->n_colnodes, 1) * sizeof(int32_t), st));
-    if (nn) {
+    if (nn && fast) {
+        SA_LAUNCH((k_node_symbolic<D, true>), grid_for(nn, NS_THREADS), NS_THREADS, 0, st, (const I *)M->me,
+                  P->inc_ptr, P->inc, nn, cnt, (const int64_t *)P->colptr, P->cols,
+                  (unsigned long long *)(P->counters + 7));
+    } else if (nn) {
         SA_LAUNCH(k_node_cols<D>, grid_for(nn, 128), 128, 0, st, (const I *)M->me, P->inc_ptr, P->inc, nn, cnt,
                   (const int64_t *)P->colptr, P->cols, (unsigned long long *)(P->counters + 5));
         SA_LAUNCH(k_inc_ranks<D>, grid_for(nn, 128), 128, 0, st, (const I *)M->me, P->inc_ptr, P->inc, nn, P->colptr,

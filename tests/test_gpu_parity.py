@@ -58,8 +58,12 @@ def _oracle(mesh, kind, nthreads=16, **kw):
     return O.assemble(mesh.q, mesh.me, op, nthreads=nthreads)
 
 
+@pytest.mark.parametrize("symfast", ["1", "0"])
 @pytest.mark.parametrize("d,n", [(2, 200), (3, 40)])
-def test_fused_mass_stiffness_vs_oracle(cuda_ok, d, n):
+def test_fused_mass_stiffness_vs_oracle(cuda_ok, d, n, symfast, monkeypatch):
+    # symfast: the fused shared-memory symbolic node pass (default) and the
+    # general symbolic kernels give the same plan
+    monkeypatch.setenv("SA_SYMFAST", symfast)
     # C1 is d=2, n=200 (configs[0]); fused numeric pass, two outputs
     mesh = _jittered(d, n, 14013301)
     mass, stiff = P.assemble_many_b200(mesh, [P.MassKernel(mesh), P.StiffnessKernel(mesh)])

@@ -1,8 +1,10 @@
 #!/bin/bash
 # Round evidence: tests, smoke, full bench (C2 + e2e + cpu baseline), per-config
-# numeric benches, launch list and one full ncu capture of the numeric kernel.
+# numeric benches, full-size parity, the C2 launch list and one full ncu
+# capture of every numeric kernel per config.  TAG names the captures.
 cd "${GRAFT_REPO_ROOT:-$(dirname $0)/..}"
 mkdir -p gpurun_out
+TAG=${TAG:-r01}
 make -s -C oracle
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/ev_pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/ev_pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/ev_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/ev_smoke.log
@@ -13,7 +15,7 @@ timeout 900 python bench.py --config C5 --steps 5 --warmup 3 --no-cpu-baseline >
 timeout 1800 python tools/fullsize_parity.py C1 C2 C3 C4 C5 > gpurun_out/ev_fullsize_parity.log 2>&1; echo "parity rc=$?" >> gpurun_out/ev_fullsize_parity.log
 CMD="python bench.py --config C2 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/ev_plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ev_launches_C2.csv $CMD > gpurun_out/ev_ncu1.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_numeric -s 3 -c 1 -o gpurun_out/ev_prof_C2 -f $CMD > gpurun_out/ev_ncu2.log 2>&1
-echo "ncu rc=$?"
-tail -1 gpurun_out/ev_pytest_gpu.log; tail -1 gpurun_out/ev_smoke.log
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_C2_${TAG}.csv $CMD > gpurun_out/ev_ncu1.log 2>&1
+echo "launches rc=$?"
+for c in ${PROF_CFGS:-C1 C2 C3 C4 C5}; do CFG=$c TAG=$TAG bash tools/prof_cfg.sh; done
+tail -n 1 gpurun_out/ev_pytest_gpu.log; tail -n 1 gpurun_out/ev_smoke.log
