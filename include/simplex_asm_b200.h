@@ -123,6 +123,13 @@ typedef struct sa_coeffs {
 int sa_numeric(sa_plan *plan, int ops, const sa_coeffs *coeffs, double *const *vals_dev,
                int64_t *n_zero_out, void *stream);
 
+/* Optional: build the per-plan structures the numeric kernel selected for
+ * `ops` needs (the two-pass slot map, local-row buffer and element batches
+ * of the 3D general operator) now instead of on the first sa_numeric call,
+ * so that they are accounted to the symbolic phase.  No reference
+ * counterpart (the reference re-sorts on every assembly). */
+int sa_plan_prepare(sa_plan *plan, int ops, void *stream);
+
 /* Drop exact-zero entries (sparse.py:108-111) from one op's values:
  * writes the canonical block CSR (indptr_out relative int64, indices_out
  * int32, vals_out f64, sized from sa_numeric's n_zero). */

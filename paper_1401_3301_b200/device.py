@@ -209,6 +209,16 @@ class Plan:
                 del d
         return c, keep
 
+    def prepare(self, kernels, stream=None):
+        """Build the per-plan structures the numeric kernel for these
+        kernels needs (two-pass slot map / row buffer / element batches)
+        now, so they count as symbolic work (sa_plan_prepare)."""
+        ops = 0
+        for k in kernels:
+            ops |= OP_BITS[k.op]
+        with torch.cuda.device(self.dmesh.device):
+            _lib.check(_lib.load().sa_plan_prepare(self._h, ops, _stream_ptr(stream)))
+
     def resident_coeffs(self, kernels):
         """Upload the kernels' nodal coefficients once and keep them in HBM;
         pass the result as ``numeric(..., coeffs=...)`` to re-assemble without
