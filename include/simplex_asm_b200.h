@@ -64,6 +64,11 @@ typedef struct sa_plan sa_plan;   /* symbolic phase for one dof-row block       
  * The mesh keeps private device copies (q as padded AoS, me as int32). */
 int sa_mesh_create(int d, int64_t nq, int64_t nme, const double *q_dev, const int64_t *me_dev,
                    const double *vols_dev, int core, int device, void *stream, sa_mesh **out);
+/* q_dev may be NULL in sa_mesh_create: the connectivity is packed and the
+ * symbolic phase (which needs only me) can run while the coordinates are
+ * still uploading; sa_mesh_set_coords then packs q and copies / computes
+ * vols (as sa_mesh_create would).  sa_numeric fails until they are set. */
+int sa_mesh_set_coords(sa_mesh *mesh, const double *q_dev, const double *vols_dev, void *stream);
 int sa_mesh_vols(const sa_mesh *mesh, double *vols_dev_out, void *stream);
 int sa_mesh_destroy(sa_mesh *mesh);
 

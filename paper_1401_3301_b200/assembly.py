@@ -61,51 +61,74 @@ def _as_descriptor(mesh, kernel):
                     "paper_1401_3301_b200.{MassKernel,StiffnessKernel,ElasticKernel,GeneralKernel}")
 
 
+class _PatternDownload:
+    """Asynchronous device->host copy of one block pattern: indptr (int64)
+    and the column indices as int32 (half the PCIe bytes of int64; widened
+    on the host, sparse.py:53-55 stores int64), on a side stream so it can
+    overlap the numeric phase.  ``col_offset`` shifts a slab's local columns
+    to global dofs on the device first."""
+
+    def __init__(self, indptr, indices, col_offset: int = 0):
+        import torch
+
+        self.key = (indptr.data_ptr(), indices.data_ptr(), indices.numel())
+        self.stream = torch.cuda.Stream(device=indptr.device)
+        self.stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.stream):
+            ix = indices + col_offset if col_offset else indices
+            self.ip = torch.empty(indptr.shape, dtype=torch.int64, pin_memory=True)
+            self.ix32 = torch.empty(ix.shape, dtype=torch.int32, pin_memory=True)
+            self.ip.copy_(indptr, non_blocking=True)
+            self.ix32.copy_(ix, non_blocking=True)
+            self.done = torch.cuda.Event()
+            self.done.record(self.stream)
+        self._host = None
+
+    def host(self):
+        """(row_ptr int64, col_idx int64) numpy arrays; waits for this copy
+        only, then widens on the host (torch's parallel CPU copy) while other
+        transfers continue."""
+        import torch
+
+        if self._host is None:
+            self.done.synchronize()
+            ix64 = torch.empty(self.ix32.shape, dtype=torch.int64, pin_memory=True)
+            ix64.copy_(self.ix32)
+            self._host = (self.ip.numpy(), ix64.numpy())
+        return self._host
+
+
 def to_host(csr: DeviceCSR, nrows_total: int | None = None) -> SparseMatrix:
     """Download a full-matrix device CSR into the reference's SparseMatrix
     (int64 indices, as sparse.py:53-55)."""
-    import torch
-
-    nrows = csr.row_end - csr.row_begin if nrows_total is None else nrows_total
-    # int32 -> int64 on the device (SparseMatrix stores int64, sparse.py:53-55),
-    # then one asynchronous copy per array into pinned host buffers
-    srcs = (csr.indptr, csr.indices.to(torch.int64), csr.vals)
-    outs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in srcs]
-    for o, t in zip(outs, srcs):
-        o.copy_(t, non_blocking=True)
-    torch.cuda.current_stream().synchronize()
-    row_ptr, col_idx, vals = (o.numpy() for o in outs)
-    return SparseMatrix(nrows, csr.ncols, row_ptr, col_idx, vals)
+    return to_host_many([csr], nrows_total)[0]
 
 
-def to_host_many(csrs, nrows_total=None, col_offset: int = 0) -> list[SparseMatrix]:
+def to_host_many(csrs, nrows_total=None, col_offset: int = 0, patterns=()) -> list[SparseMatrix]:
     """Download several results; fused outputs that share one pattern (no
     exact-zero entries dropped) share the host row_ptr/col_idx arrays, so the
-    pattern crosses PCIe once.  ``col_offset`` is added to the column indices
-    on the device (a slab's local columns -> global dofs)."""
+    pattern crosses PCIe once (as int32 indices, widened on the host while
+    the values transfer).  ``col_offset`` is added to the column indices on
+    the device (a slab's local columns -> global dofs).  ``patterns``:
+    downloads already in flight (_PatternDownload)."""
     import torch
 
-    cache = {}
-    out = []
+    cache = {p.key: p for p in patterns}
     for c in csrs:
         key = (c.indptr.data_ptr(), c.indices.data_ptr(), c.indices.numel())
         if key not in cache:
-            ix = c.indices.to(torch.int64)
-            if col_offset:
-                ix += col_offset
-            srcs = (c.indptr, ix)
-            pinned = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in srcs]
-            for o, t in zip(pinned, srcs):
-                o.copy_(t, non_blocking=True)
-            cache[key] = pinned
+            cache[key] = _PatternDownload(c.indptr, c.indices, col_offset)
+    vals = []
+    for c in csrs:
         v = torch.empty(c.vals.shape, dtype=c.vals.dtype, pin_memory=True)
         v.copy_(c.vals, non_blocking=True)
-        out.append((c, cache[key], v))
-    torch.cuda.current_stream().synchronize()
+        vals.append(v)
     res = []
-    for c, (ip, ix), v in out:
+    hosts = [cache[(c.indptr.data_ptr(), c.indices.data_ptr(), c.indices.numel())].host() for c in csrs]
+    torch.cuda.current_stream().synchronize()
+    for c, (ip, ix), v in zip(csrs, hosts, vals):
         nrows = c.row_end - c.row_begin if nrows_total is None else nrows_total
-        res.append(SparseMatrix(nrows, c.ncols, ip.numpy(), ix.numpy(), v.numpy()))
+        res.append(SparseMatrix(nrows, c.ncols, ip, ix, v.numpy()))
     return res
 
 
@@ -140,15 +163,31 @@ def assemble_block_b200(mesh, kernels, row_begin: int, row_end: int, core: str =
 
     kernels = [_as_descriptor(mesh, k) for k in kernels]
     t = time.perf_counter()
-    dm = DeviceMesh(mesh.q, mesh.me, getattr(mesh, "vols", None), core=core)
-    torch.cuda.current_stream().synchronize()
+    # connectivity first (the symbolic phase needs only it); the coordinates
+    # and volumes upload on a side stream while the symbolic phase runs
+    # (and volumes: the 3D records carry them)
+    main = torch.cuda.current_stream()
+    med = torch.as_tensor(np.asarray(mesh.me)).to(main.device, non_blocking=True)
+    vols = getattr(mesh, "vols", None)
+    vd = torch.as_tensor(np.asarray(vols)).to(main.device, non_blocking=True) if vols is not None else None
+    me_done = torch.cuda.Event()
+    me_done.record(main)
+    side = torch.cuda.Stream(device=main.device)
+    side.wait_event(me_done)
+    with torch.cuda.stream(side):
+        qd = torch.as_tensor(np.asarray(mesh.q)).to(main.device, non_blocking=True)
+    dm = DeviceMesh(None, med, vd, core=core, nq=int(np.asarray(mesh.q).shape[1]))
     t1 = time.perf_counter()
     plan = dm.plan(kernels[0].m, row_begin, row_end)
+    main.wait_stream(side)
+    dm.set_coords(qd)
+    # the structural pattern downloads while the numeric phase runs
+    pat = _PatternDownload(*plan.pattern(), col_offset)
     t2 = time.perf_counter()
     csrs = plan.assemble(kernels)
     torch.cuda.current_stream().synchronize()
     t3 = time.perf_counter()
-    out = to_host_many(csrs, col_offset=col_offset)
+    out = to_host_many(csrs, col_offset=col_offset, patterns=(pat,))
     t4 = time.perf_counter()
     dm.close()
     if timings is not None:

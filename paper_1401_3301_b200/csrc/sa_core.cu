@@ -33,6 +33,8 @@ struct sa_mesh {
     void *me = nullptr;   // IdxT<d>[nme]  (int32 AoS, one 16 B load per element)
     double *vols = nullptr;
     int64_t *scratch = nullptr;  // [0] bad index
+    bool coords = false;         // q packed and vols set (sa_mesh_create with q, or sa_mesh_set_coords)
+    bool vols_ready = false;     // vols set (the 3D symbolic phase copies them into its records)
 };
 
 // Warp-interleaved incidence record (row-gather kernel): everything an
@@ -1675,6 +1677,9 @@ __global__ void k_compact(const int64_t *__restrict__ indptr, const int32_t *__r
 // dispatch helpers
 
 template <int D>
+int mesh_coords(sa_mesh *M, const double *q, const double *vols, cudaStream_t st);
+
+template <int D>
 int mesh_kernels(sa_mesh *M, const double *q, const int64_t *me, const double *vols, cudaStream_t st)
 {
     typedef typename VecT<D>::type V;
@@ -1684,7 +1689,7 @@ int mesh_kernels(sa_mesh *M, const double *q, const int64_t *me, const double *v
     const int B = 256;
     unsigned gq = std::min<int64_t>(grid_for(M->nq, B), 148 * 32);
     unsigned ge = std::min<int64_t>(grid_for(M->nme, B), 148 * 32);
-    if (M->nq) SA_LAUNCH(k_pack_q<D>, gq, B, 0, st, q, M->nq, (V *)M->qv);
+    if (M->nq && q) SA_LAUNCH(k_pack_q<D>, gq, B, 0, st, q, M->nq, (V *)M->qv);
     if (M->nme) SA_LAUNCH(k_pack_me<D>, ge, B, 0, st, me, M->nq, M->nme, (I *)M->me, bad);
     unsigned long long hbad = 0;
     SA_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, st));
@@ -1694,6 +1699,31 @@ int mesh_kernels(sa_mesh *M, const double *q, const int64_t *me, const double *v
         return set_error(SA_ERR_INDEX_RANGE, "connectivity entry me[%lld, %lld] out of range [0, %lld)",
                          (long long)(hbad / M->nme), (long long)(hbad % M->nme), (long long)M->nq);
     }
+    if (!q) {   // coordinates later (sa_mesh_set_coords); given volumes now
+        if (vols) {
+            SA_CUDA_TRY(cudaMemcpyAsync(M->vols, vols, M->nme * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            M->vols_ready = true;
+        }
+        return SA_OK;
+    }
+    return mesh_coords<D>(M, nullptr, vols, st);
+}
+
+// q (if given) packed to AoS, then vols copied or computed on the device
+template <int D>
+int mesh_coords(sa_mesh *M, const double *q, const double *vols, cudaStream_t st)
+{
+    typedef typename VecT<D>::type V;
+    typedef typename IdxT<D>::type I;
+    unsigned long long *bad = (unsigned long long *)M->scratch;
+    unsigned long long hbad = 0;
+    const int B = 256;
+    unsigned gq = std::min<int64_t>(grid_for(M->nq, B), 148 * 32);
+    unsigned ge = std::min<int64_t>(grid_for(M->nme, B), 148 * 32);
+    if (M->nq && q) SA_LAUNCH(k_pack_q<D>, gq, B, 0, st, q, M->nq, (V *)M->qv);
+    M->coords = true;
+    if (M->vols_ready) return SA_OK;
+    M->vols_ready = true;
     if (vols) {
         SA_CUDA_TRY(cudaMemcpyAsync(M->vols, vols, M->nme * sizeof(double), cudaMemcpyDeviceToDevice, st));
     } else if (M->nme) {
@@ -2050,7 +2080,9 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
     // (they replace three dependent gathers per incidence; measured faster),
     // off in 1D/2D (same speed there, 4x the record traffic); SA_WINC=0|1
     const char *wi_s = getenv("SA_WINC");
-    const bool want_winc = wi_s ? atoi(wi_s) != 0 : D == 3;
+    // (the records carry the volume: without it yet -- a mesh created
+    // without coordinates or volumes -- the plan uses the 8-byte records)
+    const bool want_winc = (wi_s ? atoi(wi_s) != 0 : D == 3) && M->vols_ready;
     if (nn && want_winc) {
         const int64_t nw = (nn + 31) / 32;
         SA_CUDA_TRY(cudaMallocAsync((void **)&P->wseg, (nw + 1) * sizeof(int64_t), st));
@@ -2306,6 +2338,9 @@ int dispatch_numeric(const sa_plan *P, const NumArgs &a, int ops, int core, cuda
 int sa_mesh_kernels_d1(sa_mesh *, const double *, const int64_t *, const double *, cudaStream_t);
 int sa_mesh_kernels_d2(sa_mesh *, const double *, const int64_t *, const double *, cudaStream_t);
 int sa_mesh_kernels_d3(sa_mesh *, const double *, const int64_t *, const double *, cudaStream_t);
+int sa_mesh_coords_d1(sa_mesh *, const double *, const double *, cudaStream_t);
+int sa_mesh_coords_d2(sa_mesh *, const double *, const double *, cudaStream_t);
+int sa_mesh_coords_d3(sa_mesh *, const double *, const double *, cudaStream_t);
 int sa_symbolic_d1(sa_plan *, cudaStream_t);
 int sa_symbolic_d2(sa_plan *, cudaStream_t);
 int sa_symbolic_d3(sa_plan *, cudaStream_t);
@@ -2318,6 +2353,10 @@ int SA_CAT(sa_mesh_kernels_d, SA_D)(sa_mesh *M, const double *q, const int64_t *
     return mesh_kernels<SA_D>(M, q, me, vols, st);
 }
 int SA_CAT(sa_symbolic_d, SA_D)(sa_plan *P, cudaStream_t st) { return symbolic_kernels<SA_D>(P, st); }
+int SA_CAT(sa_mesh_coords_d, SA_D)(sa_mesh *M, const double *q, const double *vols, cudaStream_t st)
+{
+    return mesh_coords<SA_D>(M, q, vols, st);
+}
 int SA_CAT(sa_dispatch_d, SA_D)(const sa_plan *P, const NumArgs &a, int ops, int core, cudaStream_t st)
 {
     return dispatch_numeric<SA_D>(P, a, ops, core, st);
@@ -2394,6 +2433,16 @@ int sa_mesh_create(int d, int64_t nq, int64_t nme, const double *q_dev, const in
     if (rc != SA_OK) return fail(rc);
     *out = M;
     return SA_OK;
+}
+
+int sa_mesh_set_coords(sa_mesh *M, const double *q_dev, const double *vols_dev, void *stream)
+{
+    if (!M || !q_dev) return set_error(SA_ERR_ARG, "mesh/q is NULL");
+    SA_TRY(set_device(M->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    if (M->d == 1) return sa_mesh_coords_d1(M, q_dev, vols_dev, st);
+    if (M->d == 2) return sa_mesh_coords_d2(M, q_dev, vols_dev, st);
+    return sa_mesh_coords_d3(M, q_dev, vols_dev, st);
 }
 
 int sa_mesh_vols(const sa_mesh *M, double *vols_dev_out, void *stream)
@@ -2595,6 +2644,7 @@ int sa_numeric(sa_plan *P, int ops, const sa_coeffs *cf, double *const *vals_dev
 {
     if (!P || !vals_dev) return set_error(SA_ERR_ARG, "plan/vals is NULL");
     const sa_mesh *M = P->mesh;
+    if (!M->coords) return set_error(SA_ERR_ARG, "mesh coordinates not set (sa_mesh_set_coords)");
     const int d = M->d;
     if ((ops & SA_OP_ELASTIC) && P->m != d) return set_error(SA_ERR_ARG, "elastic operator needs a plan with m = d");
     if (!(ops & SA_OP_ELASTIC) && P->m != 1) return set_error(SA_ERR_ARG, "scalar operators need a plan with m = 1");

@@ -53,16 +53,19 @@ class DeviceMesh:
     layout) or CUDA tensors.  ``vols=None`` computes volumes on the device.
     """
 
-    def __init__(self, q, me, vols=None, *, core: str = "SkylakeX", device=None, stream=None):
+    def __init__(self, q, me, vols=None, *, core: str = "SkylakeX", device=None, stream=None, nq: int | None = None):
         dev = _require_cuda(device)
         L = _lib.load()
         self.device = dev
         self.core = core
         with torch.cuda.device(dev):
-            qd = _to_dev(q, torch.float64, dev)
+            # q=None (with nq): connectivity only; set_coords() later -- the
+            # symbolic phase can run while the coordinates upload
+            qd = _to_dev(q, torch.float64, dev) if q is not None else None
             med = _to_dev(me, torch.int64, dev)
             vd = _to_dev(vols, torch.float64, dev) if vols is not None else None
-            self.d, self.nq = int(qd.shape[0]), int(qd.shape[1])
+            self.d = int(med.shape[0]) - 1 if qd is None else int(qd.shape[0])
+            self.nq = int(nq) if qd is None else int(qd.shape[1])
             self.nme = int(med.shape[1]) if med.dim() == 2 else 0
             if med.shape[0] != self.d + 1:
                 raise ValueError(f"connectivity shape {tuple(med.shape)} does not match ({self.d + 1}, nme)")
@@ -76,6 +79,14 @@ class DeviceMesh:
     @property
     def handle(self):
         return self._h
+
+    def set_coords(self, q, vols=None, stream=None):
+        """Coordinates (and volumes; computed on the device when None) of a
+        mesh created with q=None (sa_mesh_set_coords)."""
+        with torch.cuda.device(self.device):
+            qd = _to_dev(q, torch.float64, self.device)
+            vd = _to_dev(vols, torch.float64, self.device) if vols is not None else None
+            _lib.check(_lib.load().sa_mesh_set_coords(self._h, _ptr(qd), _ptr(vd), _stream_ptr(stream)))
 
     def vols(self, stream=None) -> "torch.Tensor":
         out = torch.empty(self.nme, dtype=torch.float64, device=self.device)

@@ -246,3 +246,29 @@ def test_high_valence_node(cuda_ok, k):
     mesh = P.Mesh(q, me, O.volumes(q, me))
     got = P.assemble_b200(mesh, P.StiffnessKernel(mesh))
     assert_csr_equal(got, *_oracle(mesh, "stiffness", nthreads=1))
+
+
+@pytest.mark.parametrize("d,n,parts", [(2, 40, 3), (3, 9, 2)])
+def test_block_e2e_slabs_stitch_bitwise(cuda_ok, d, n, parts):
+    # the public per-rank call (assemble_block_b200: connectivity first,
+    # coordinates uploaded during the symbolic phase, pattern downloaded
+    # during the numeric phase, int32 indices widened on the host) on each
+    # rank's slab stitches to the full oracle matrices, bitwise
+    from oracle import oracle as O
+    from paper_1401_3301_b200 import parallel
+    from paper_1401_3301_b200.assembly import assemble_block_b200
+
+    mesh = _jittered(d, n, 21)
+    nq = mesh.q.shape[1]
+    blocks_m, blocks_s = [], []
+    for rb, re_ in parallel.row_blocks(nq, 1, parts):
+        sl = parallel.slab(mesh.q, mesh.me, 1, rb, re_, mesh.vols)
+        smesh = P.Mesh(sl.q, sl.me, sl.vols)
+        ms, st = assemble_block_b200(smesh, [P.MassKernel(smesh), P.StiffnessKernel(smesh)], sl.row_begin,
+                                     sl.row_end, col_offset=sl.col_offset)
+        assert ms.col_idx.dtype == np.int64
+        blocks_m.append((rb, re_, ms.row_ptr, ms.col_idx, ms.vals))
+        blocks_s.append((rb, re_, st.row_ptr, st.col_idx, st.vals))
+    assert_csr_equal(P.SparseMatrix(nq, nq, *parallel.stitch(blocks_m, nq, nq)),
+                     *_oracle(mesh, "mass", w=np.ones(nq)))
+    assert_csr_equal(P.SparseMatrix(nq, nq, *parallel.stitch(blocks_s, nq, nq)), *_oracle(mesh, "stiffness"))
