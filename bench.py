@@ -268,6 +268,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the numeric phase directly instead of "
+                    "replaying its CUDA graph")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N > 1: weak = per-GPU work fixed (refined global mesh), strong = the config mesh split N ways")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -357,6 +359,12 @@ def main():
         plan.numeric(kernels, out=out, sync=False, coeffs=resident)
     vals, zeros = plan.numeric(kernels, out=out, sync=True, coeffs=resident)  # raises on degenerate input
     torch.cuda.synchronize()
+    # one numeric step = one CUDA-graph replay of sa_numeric's launches
+    # (--no-graph: direct launches through the C ABI every step)
+    graph = None if args.no_graph else plan.numeric_graph(kernels, out, resident)
+    for _ in range(2 if graph is not None else 0):
+        graph.replay()
+    torch.cuda.synchronize()
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -368,11 +376,16 @@ def main():
         for i in range(args.steps):
             flush.fill_(float(i))           # L2 flush between timed steps (outside the events)
             starts[i].record()
-            plan.numeric(kernels, out=out, sync=False, coeffs=resident)
+            if graph is not None:
+                graph.replay()
+            else:
+                plan.numeric(kernels, out=out, sync=False, coeffs=resident)
             ends[i].record()
         torch.cuda.synchronize()
         time.sleep(0.12)
     launches = D.launch_count()
+    if graph is not None:   # kernels launched by the replays (captured once, counted per replay)
+        launches += graph.sa_kernels_per_replay * args.steps
     if world > 1:
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
@@ -434,7 +447,8 @@ def main():
                             if k in ("incidences", "max_row_nodes", "nodes", "nnz") or v},
                    "kernel": os.environ.get("SA_KERNEL", "default"),
                    "l2": "flushed between timed steps (256 MiB write); inputs+outputs > L2",
-                   "timing": "per-step CUDA events on the launching stream, summed; max over ranks"},
+                   "timing": "per-step CUDA events on the launching stream, summed; max over ranks",
+                   "launch": "CUDA graph replay of the numeric phase" if graph is not None else "direct"},
         "nnz_per_s": nnz_struct_all * len(kernels) / (ms_per_step * 1e-3),
         "symbolic_ms": t_sym_ms,
         "symbolic_cold_ms": t_sym_cold_ms,

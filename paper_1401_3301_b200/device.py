@@ -264,6 +264,28 @@ class Plan:
         return ([by_kernel[id(k)] for k in kernels],
                 [zeros[id(k)] for k in kernels] if sync else None)
 
+    def numeric_graph(self, kernels, out, coeffs):
+        """Capture one re-assembly (sa_numeric: counter resets + the numeric
+        kernel launches, no host sync) in a CUDA graph; ``g.replay()`` then
+        re-assembles into ``out`` with one launch from the host, so small
+        meshes are not bound by per-launch host overhead.  The plan's
+        kernel-specific data must exist first (prepare() or one numeric call);
+        zero counts / degenerate checks need a regular numeric(sync=True)."""
+        self.prepare(kernels)
+        torch.cuda.synchronize(self.dmesh.device)
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=self.dmesh.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.numeric(kernels, out=out, sync=False, coeffs=coeffs)   # warm (module loads, attributes)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize(self.dmesh.device)
+        n0 = launch_count()
+        with torch.cuda.graph(g):
+            self.numeric(kernels, out=out, sync=False, coeffs=coeffs)
+        g.sa_kernels_per_replay = launch_count() - n0   # library kernels inside the graph
+        return g
+
     def compact(self, vals: "torch.Tensor", n_zero: int, stream=None) -> DeviceCSR:
         """Canonical block CSR: exact-zero sums dropped (sparse.py:108-111)."""
         ip, ix = self.pattern(stream)

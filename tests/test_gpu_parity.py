@@ -272,3 +272,34 @@ def test_block_e2e_slabs_stitch_bitwise(cuda_ok, d, n, parts):
     assert_csr_equal(P.SparseMatrix(nq, nq, *parallel.stitch(blocks_m, nq, nq)),
                      *_oracle(mesh, "mass", w=np.ones(nq)))
     assert_csr_equal(P.SparseMatrix(nq, nq, *parallel.stitch(blocks_s, nq, nq)), *_oracle(mesh, "stiffness"))
+
+
+def test_numeric_graph_replay_bitwise(cuda_ok):
+    # the CUDA-graph replay of the numeric phase (bench.py's step) writes the
+    # same values as a direct call, for the one-pass and the two-pass kernels
+    import torch
+
+    from paper_1401_3301_b200.device import OP_BITS, DeviceMesh
+
+    for d, n, ks in ((2, 60, ("mass", "stiffness")), (3, 10, ("general",))):
+        mesh = _jittered(d, n, 5)
+        nq = mesh.q.shape[1]
+        rng = np.random.default_rng(1)
+        kern = {"mass": lambda: P.MassKernel(mesh), "stiffness": lambda: P.StiffnessKernel(mesh),
+                "general": lambda: P.GeneralKernel(mesh, A=np.eye(3)[None] + 0.1 * rng.random((nq, 3, 3)),
+                                                   b=rng.random((nq, 3)), c=rng.random((nq, 3)),
+                                                   a0=rng.random(nq))}
+        kernels = [kern[k]() for k in ks]
+        plan = DeviceMesh(mesh.q, mesh.me, mesh.vols).plan(1)
+        ref, _ = plan.numeric(kernels)
+        ref = [r.clone() for r in ref]
+        out = [torch.full((plan.nnz,), float("nan"), dtype=torch.float64, device="cuda") for _ in kernels]
+        g = plan.numeric_graph(kernels, out, plan.resident_coeffs(kernels))
+        for o in out:
+            o.fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize()
+        assert g.sa_kernels_per_replay >= 1
+        order = sorted(range(len(kernels)), key=lambda i: OP_BITS[kernels[i].op])
+        for j, i in enumerate(order):
+            assert torch.equal(out[j], ref[i])
