@@ -76,8 +76,10 @@ def profiled_traffic(name):
 def make_mesh(cfg, vols_on_device=True):
     import paper_1401_3301_b200 as P
 
-    q, me = P.hypercube_arrays(cfg["d"], cfg["n"])
-    q = P.jitter_interior(q, cfg["n"], 0.2 if cfg["d"] == 2 else 0.15, cfg["seed"])
+    # generated on the B200 (sa_kuhn_mesh), bitwise the host generator's
+    # arrays (tests/test_gpu_parity.py::test_device_mesh_generator_bitwise)
+    q, me = P.device_hypercube_arrays(cfg["d"], cfg["n"], seed=cfg["seed"],
+                                      amplitude=0.2 if cfg["d"] == 2 else 0.15, host=True)
     if os.environ.get("SA_BENCH_RENUMBER") == "morton":   # locality experiment
         q, me = _morton_renumber(q, me, cfg["n"])
     return q, me

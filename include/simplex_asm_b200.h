@@ -148,6 +148,18 @@ int64_t sa_bad_index(void);
  * (bench.py's gpu_launches). */
 int64_t sa_launch_count(int reset);
 
+/* ---- benchmark meshes on the device (sa_meshgen.cu) ------------------- */
+
+/* Kuhn triangulation of [0,1]^d, n cells per axis, written to caller-owned
+ * device buffers q_dev (d, (n+1)^d) f64 and me_dev (d+1, d! n^d) int64 --
+ * bitwise the arrays of generate_hypercube_mesh (mesh.py:104-140).  With
+ * jitter != 0 the interior nodes move by numpy's
+ * default_rng(seed).uniform(lo, lo + range, size=(d, (n-1)^d)) (SURVEY.md
+ * 8(d)); (state, inc) = np.random.PCG64(seed).state after seeding.
+ * Either buffer may be NULL. */
+int sa_kuhn_mesh(int d, int64_t n, int jitter, double lo, double range, uint64_t state_hi, uint64_t state_lo,
+                 uint64_t inc_hi, uint64_t inc_lo, double *q_dev, int64_t *me_dev, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,7 +17,14 @@ from .errors import (
     SimplexAsmError,
 )
 from .kernels import ElasticKernel, GeneralKernel, MassKernel, StiffnessKernel
-from .mesh import Mesh, generate_hypercube_mesh, hypercube_arrays, jitter_interior, jittered_hypercube_mesh
+from .mesh import (
+    Mesh,
+    device_hypercube_arrays,
+    generate_hypercube_mesh,
+    hypercube_arrays,
+    jitter_interior,
+    jittered_hypercube_mesh,
+)
 from .sparse import SparseMatrix, to_scipy
 
 __version__ = "0.1.0"

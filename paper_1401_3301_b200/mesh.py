@@ -108,3 +108,45 @@ def jittered_hypercube_mesh(d: int, n: int, seed: int, amplitude: float | None =
     q, me = hypercube_arrays(d, n)
     q = jitter_interior(q, n, amplitude, seed)
     return Mesh.from_arrays(q, me, vols)
+
+
+def device_hypercube_arrays(d: int, n: int, seed: int | None = None, amplitude: float | None = None,
+                            device=None, host: bool = False):
+    """The benchmark mesh generated on the B200 (sa_kuhn_mesh): bitwise the
+    arrays of ``hypercube_arrays`` (+ ``jitter_interior`` when ``seed`` is
+    given; a = 0.2 in 2D, 0.15 in 3D unless given).  Returns CUDA tensors
+    (q (d, nq) f64, me (d+1, nme) int64), or numpy arrays when ``host``
+    (one device->host copy instead of the host generator)."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .device import _require_cuda, _stream_ptr
+
+    if d < 1 or d > 3:
+        raise ValueError(f"dimension must be 1, 2 or 3, got {d}")
+    if n < 1:
+        raise ValueError(f"subdivision count must be >= 1, got {n}")
+    dev = _require_cuda(device)
+    nq, nme = (n + 1) ** d, math.factorial(d) * n ** d
+    q = torch.empty((d, nq), dtype=torch.float64, device=dev)
+    me = torch.empty((d + 1, nme), dtype=torch.int64, device=dev)
+    lo = rg = 0.0
+    s_hi = s_lo = i_hi = i_lo = 0
+    if seed is not None:
+        if amplitude is None:
+            amplitude = 0.2 if d <= 2 else 0.15
+        h = 1.0 / n
+        lo, hi = -amplitude * h, amplitude * h     # numpy: uniform(lo, hi) = lo + (hi - lo) u
+        rg = hi - lo
+        st = np.random.PCG64(seed).state["state"]  # default_rng(seed)'s seeded generator
+        s_hi, s_lo = st["state"] >> 64, st["state"] & ((1 << 64) - 1)
+        i_hi, i_lo = st["inc"] >> 64, st["inc"] & ((1 << 64) - 1)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.load().sa_kuhn_mesh(d, n, 1 if seed is not None else 0, lo, rg, s_hi, s_lo, i_hi, i_lo,
+                                            ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(me.data_ptr()),
+                                            _stream_ptr()))
+    if host:
+        return q.cpu().numpy(), me.cpu().numpy()
+    return q, me

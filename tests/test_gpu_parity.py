@@ -303,3 +303,15 @@ def test_numeric_graph_replay_bitwise(cuda_ok):
         order = sorted(range(len(kernels)), key=lambda i: OP_BITS[kernels[i].op])
         for j, i in enumerate(order):
             assert torch.equal(out[j], ref[i])
+
+
+@pytest.mark.parametrize("d,n,seed", [(1, 37, 3), (2, 25, 14013302), (2, 1, None), (3, 7, 14013305), (3, 12, None)])
+def test_device_mesh_generator_bitwise(cuda_ok, d, n, seed):
+    # sa_kuhn_mesh (Kuhn cube + numpy-PCG64 jitter restated with jump-ahead)
+    # equals the host generator (mesh.py:104-140 + SURVEY 8(d) jitter) bit for bit
+    q_h, me_h = P.hypercube_arrays(d, n)
+    if seed is not None:
+        q_h = P.jitter_interior(q_h, n, 0.2 if d <= 2 else 0.15, seed)
+    q_d, me_d = P.device_hypercube_arrays(d, n, seed=seed, host=True)
+    assert np.array_equal(me_d, me_h)
+    assert np.array_equal(q_d.view(np.int64), q_h.view(np.int64))
