@@ -148,6 +148,27 @@ int64_t sa_bad_index(void);
  * (bench.py's gpu_launches). */
 int64_t sa_launch_count(int reset);
 
+/* ---- Pk mass matrix (order-k node lattices; csrc/sa_pk.cuh) ------------ */
+
+/* Replaces assemble_mass_pk (assembly.py:265-292): every local entry is
+ * (d! C[a][b]) * |K| with an element-independent table C.  me_dev is the
+ * lattice connectivity (ndfe, nme) int64 (PkMesh.me, mesh.py:167-192);
+ * ndfe <= 84, <= 255 distinct neighbours per node.  The symbolic plan holds
+ * the structural pattern (CSR over nq x nq); sa_pk_mass folds every entry in
+ * ascending element order (cs_dev = d! * C, row-major [a][b], computed as
+ * the reference computes dfact * C[a, b]); sa_pk_compact drops exact-zero
+ * sums (sparse.py:108-111). */
+typedef struct sa_pk_plan sa_pk_plan;
+int sa_pk_plan_create(int ndfe, int64_t nq, int64_t nme, const int64_t *me_dev, int device, void *stream,
+                      sa_pk_plan **out);
+int sa_pk_plan_info(const sa_pk_plan *plan, int64_t *nnz, int64_t *max_row_nodes);
+int sa_pk_plan_pattern(const sa_pk_plan *plan, int64_t *indptr_dev, int32_t *indices_dev, void *stream);
+int sa_pk_mass(sa_pk_plan *plan, const double *cs_dev, const double *vols_dev, double *vals_dev,
+               int64_t *n_zero_out, void *stream);
+int sa_pk_compact(const sa_pk_plan *plan, const double *vals_dev, int64_t *indptr_out, int32_t *indices_out,
+                  double *vals_out, void *stream);
+int sa_pk_plan_destroy(sa_pk_plan *plan);
+
 /* ---- benchmark meshes on the device (sa_meshgen.cu) ------------------- */
 
 /* Kuhn triangulation of [0,1]^d, n cells per axis, written to caller-owned

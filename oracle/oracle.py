@@ -234,3 +234,44 @@ def assemble(q, me, op: OracleOp, nthreads: int = 1):
         raise RuntimeError(f"or_assemble_threaded rc={rc}")
     n = nnz.value
     return _take(rp, ndof + 1, np.int64), _take(ci, n, np.int64), _take(va, n, np.float64)
+
+
+def assemble_mass_pk(me, vols, C, d: int, nq: int):
+    """Pk mass matrix, CPU restatement of assemble_mass_pk (assembly.py:265-292)
+    and its canonical constructor (sparse.py:85-133): element-major triplets
+    (beta outer, alpha inner within an element), value (d! * C[a, b]) * vol,
+    exact zeros skipped, stable sort by (row, col), left-to-right sums,
+    exact-zero sums dropped.  Returns (row_ptr, col_idx, vals).  Test
+    infrastructure only (numpy; small meshes)."""
+    me = np.asarray(me, dtype=np.int64)
+    vols = np.asarray(vols, dtype=np.float64)
+    ndfe, nme = me.shape
+    dfact = float(math.factorial(d))
+    vals = np.empty((ndfe * ndfe, nme))
+    rows = np.empty((ndfe * ndfe, nme), dtype=np.int64)
+    cols = np.empty((ndfe * ndfe, nme), dtype=np.int64)
+    l = 0
+    for b in range(ndfe):
+        for a in range(ndfe):
+            vals[l] = dfact * C[a, b] * vols
+            rows[l] = me[a]
+            cols[l] = me[b]
+            l += 1
+    v, r, c = vals.ravel(order="F"), rows.ravel(order="F"), cols.ravel(order="F")
+    keep = v != 0.0
+    v, r, c = v[keep], r[keep], c[keep]
+    order = np.lexsort((c, r))
+    v, r, c = v[order], r[order], c[order]
+    if len(v):
+        start = np.ones(len(v), dtype=bool)
+        start[1:] = (r[1:] != r[:-1]) | (c[1:] != c[:-1])
+        seg = np.cumsum(start) - 1
+        sums = np.bincount(seg, weights=v)
+        r, c = r[start], c[start]
+        nzs = sums != 0.0
+        r, c, sums = r[nzs], c[nzs], sums[nzs]
+    else:
+        sums = v
+    row_ptr = np.zeros(nq + 1, dtype=np.int64)
+    np.cumsum(np.bincount(r, minlength=nq), out=row_ptr[1:])
+    return row_ptr, c, sums

@@ -25,6 +25,7 @@ from .mesh import (
     jitter_interior,
     jittered_hypercube_mesh,
 )
+from .pk import PkCoeffTable, PkMesh, build_pk_mesh, multi_index_lattice, pk_mass_coeffs
 from .sparse import SparseMatrix, to_scipy
 
 __version__ = "0.1.0"
@@ -33,7 +34,8 @@ __version__ = "0.1.0"
 def __getattr__(name):
     # the device layer imports torch and loads the sm_100a library lazily
     if name in ("assemble_b200", "assemble_vector_b200", "assemble_many_b200", "assemble_device",
-                "SCALAR_DRIVERS", "VECTOR_DRIVERS", "register", "to_host", "device_mesh_for"):
+                "SCALAR_DRIVERS", "VECTOR_DRIVERS", "register", "to_host", "device_mesh_for",
+                "assemble_mass_pk_b200"):
         from . import assembly
 
         return getattr(assembly, name)

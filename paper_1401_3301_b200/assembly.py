@@ -212,6 +212,63 @@ def assemble_vector_b200(mesh, kernel) -> SparseMatrix:
     return to_host(assemble_device(mesh, [k])[0])
 
 
+def assemble_mass_pk_b200(pkmesh, coeffs) -> SparseMatrix:
+    """Pk mass matrix, same contract as assemble_mass_pk (assembly.py:265-292):
+    every local entry is (d! C[a][b]) |K|; canonical CSR, each entry summed in
+    ascending element order (bitwise the reference's values), exact-zero sums
+    dropped.  Accepts the reference's PkMesh / PkCoeffTable or this package's
+    (pk.build_pk_mesh, pk.pk_mass_coeffs)."""
+    import ctypes
+    import math
+
+    import torch
+
+    from . import _lib
+    from .device import DeviceCSR, _ptr, _require_cuda, _stream_ptr, _to_dev
+
+    if (pkmesh.d, pkmesh.k) != (coeffs.d, coeffs.k):
+        raise ValueError(
+            f"coefficient table (d={coeffs.d}, k={coeffs.k}) does not match "
+            f"lattice mesh (d={pkmesh.d}, k={pkmesh.k})"
+        )
+    dev = _require_cuda(None)
+    L = _lib.load()
+    me = np.asarray(pkmesh.me)
+    ndfe, nme = int(me.shape[0]), int(me.shape[1])
+    nq = int(np.asarray(pkmesh.q).shape[1])
+    # d! * C[a, b] exactly as the reference forms it (a float64 product)
+    cs = float(math.factorial(pkmesh.d)) * np.asarray(coeffs.C, dtype=np.float64)
+    with torch.cuda.device(dev):
+        med = _to_dev(me, torch.int64, dev)
+        vd = _to_dev(np.asarray(pkmesh.vols), torch.float64, dev)
+        csd = _to_dev(np.ascontiguousarray(cs), torch.float64, dev)
+        h = ctypes.c_void_p()
+        _lib.check(L.sa_pk_plan_create(ndfe, nq, nme, _ptr(med), dev.index, _stream_ptr(), ctypes.byref(h)))
+        try:
+            nnz, md = ctypes.c_int64(), ctypes.c_int64()
+            _lib.check(L.sa_pk_plan_info(h, ctypes.byref(nnz), ctypes.byref(md)))
+            n = nnz.value
+            ip = torch.empty(nq + 1, dtype=torch.int64, device=dev)
+            ix = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+            va = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+            _lib.check(L.sa_pk_plan_pattern(h, _ptr(ip), _ptr(ix), _stream_ptr()))
+            nz = ctypes.c_int64()
+            _lib.check(L.sa_pk_mass(h, _ptr(csd), _ptr(vd), _ptr(va), ctypes.byref(nz), _stream_ptr()))
+            if nz.value:
+                m = n - nz.value
+                nip = torch.empty(nq + 1, dtype=torch.int64, device=dev)
+                nix = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+                nva = torch.empty(max(m, 1), dtype=torch.float64, device=dev)
+                _lib.check(L.sa_pk_compact(h, _ptr(va), _ptr(nip), _ptr(nix), _ptr(nva), _stream_ptr()))
+                csr = DeviceCSR(0, nq, nq, nip, nix[:m], nva[:m])
+            else:
+                csr = DeviceCSR(0, nq, nq, ip, ix[:n], va[:n])
+            return to_host(csr)
+        finally:
+            torch.cuda.current_stream().synchronize()
+            L.sa_pk_plan_destroy(h)
+
+
 SCALAR_DRIVERS = {"b200": assemble_b200}
 VECTOR_DRIVERS = {"b200": assemble_vector_b200}
 

@@ -2738,4 +2738,6 @@ int sa_compact(const sa_plan *P, const double *vals_dev, int64_t *indptr_out, in
 }
 
 }  // extern "C"
+
+#include "sa_pk.cuh"
 #endif  // SA_ABI

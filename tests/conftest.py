@@ -17,7 +17,10 @@ def pytest_configure(config):
 
 
 def golden_cases(prefix=""):
-    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, prefix + "*.npz")))
+    """P1 fixtures (make_golden.py); prefix "pk_" selects the Pk mass ones
+    (make_golden_pk.py)."""
+    names = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, prefix + "*.npz")))
+    return names if prefix.startswith("pk_") else [n for n in names if not n.startswith("pk_")]
 
 
 def load_golden(name):

@@ -315,3 +315,33 @@ def test_device_mesh_generator_bitwise(cuda_ok, d, n, seed):
     q_d, me_d = P.device_hypercube_arrays(d, n, seed=seed, host=True)
     assert np.array_equal(me_d, me_h)
     assert np.array_equal(q_d.view(np.int64), q_h.view(np.int64))
+
+
+@pytest.mark.parametrize("name", golden_cases("pk_"))
+def test_pk_mass_golden_bitwise(cuda_ok, name):
+    # Pk mass on the B200 vs the reference's assemble_mass_pk, bitwise, with
+    # the lattice mesh and table from this package's host restatements
+    from paper_1401_3301_b200 import pk
+
+    g = load_golden(name)
+    d, k = g["q"].shape[0], int(g["k"])
+    pm = pk.build_pk_mesh(P.Mesh(g["p1_q"], g["p1_me"], g["vols"]), k)
+    got = P.assemble_mass_pk_b200(pm, pk.pk_mass_coeffs(d, k))
+    assert got.shape == tuple(g["shape"])
+    assert_csr_equal(got, g["row_ptr"], g["col_idx"], g["vals"])
+
+
+def test_pk_mass_larger_mesh_vs_oracle(cuda_ok):
+    # P2 on a 3D jittered cube (exact-zero table entries, skipped/dropped as
+    # the reference does) and P3 in 2D, against the oracle restatement
+    from oracle import oracle as O
+    from paper_1401_3301_b200 import pk
+
+    for d, n, k in ((3, 8, 2), (2, 20, 3)):
+        mesh = _jittered(d, n, 4)
+        pm = pk.build_pk_mesh(mesh, k)
+        C = pk.pk_mass_coeffs(d, k)
+        got = P.assemble_mass_pk_b200(pm, C)
+        assert_csr_equal(got, *O.assemble_mass_pk(pm.me, pm.vols, C.C, d, pm.nq))
+    with pytest.raises(ValueError):
+        P.assemble_mass_pk_b200(pm, pk.pk_mass_coeffs(d, 2))

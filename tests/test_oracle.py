@@ -58,3 +58,25 @@ def test_degenerate_element_named():
     with pytest.raises(O.OracleDegenerate) as ei:
         O.gradients(q, me)
     assert ei.value.element == 1
+
+
+def test_pk_host_restatements_and_oracle_match_reference_goldens():
+    # lattice, coefficient table, lattice mesh (host restatements in the
+    # package) and the Pk mass oracle (oracle/) against fixtures the reference
+    # itself produced (tests/golden/make_golden_pk.py) -- bitwise
+    import paper_1401_3301_b200 as P
+    from oracle import oracle as O
+    from paper_1401_3301_b200 import pk
+
+    names = golden_cases("pk_")
+    assert len(names) >= 6
+    for name in names:
+        g = load_golden(name)
+        d, k = g["q"].shape[0], int(g["k"])
+        C = pk.pk_mass_coeffs(d, k)
+        assert np.array_equal(C.C, g["C"]) and C.lattice == tuple(map(tuple, g["lattice"]))
+        pm = pk.build_pk_mesh(P.Mesh(g["p1_q"], g["p1_me"], g["vols"]), k)
+        assert np.array_equal(pm.me, g["me"]) and np.array_equal(pm.q, g["q"])
+        rp, ci, va = O.assemble_mass_pk(g["me"], g["vols"], g["C"], d, g["q"].shape[1])
+        assert np.array_equal(rp, g["row_ptr"]) and np.array_equal(ci, g["col_idx"])
+        assert np.array_equal(va, g["vals"])
