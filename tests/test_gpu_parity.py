@@ -345,3 +345,30 @@ def test_pk_mass_larger_mesh_vs_oracle(cuda_ok):
         assert_csr_equal(got, *O.assemble_mass_pk(pm.me, pm.vols, C.C, d, pm.nq))
     with pytest.raises(ValueError):
         P.assemble_mass_pk_b200(pm, pk.pk_mass_coeffs(d, 2))
+
+
+@pytest.mark.parametrize("kernel", ["rowgather", "twopass"])
+def test_haswell_core_vs_oracle(cuda_ok, kernel, monkeypatch):
+    # the OpenBLAS Haswell kernel family (unfused getrf/getrs updates,
+    # SURVEY.md Appendix A): GPU gradients and the oracle agree bitwise, so
+    # the value-dependent pattern (exact zeros) matches under that core too
+    from oracle import oracle as O
+    from paper_1401_3301_b200.assembly import to_host
+    from paper_1401_3301_b200.device import DeviceMesh
+
+    monkeypatch.setenv("SA_KERNEL", kernel)
+    mesh = _jittered(3, 9, 17)
+    nq = mesh.q.shape[1]
+    for kind in ("stiffness", "general"):
+        kw = {}
+        kern = P.StiffnessKernel(mesh)
+        if kind == "general":
+            rng = np.random.default_rng(2)
+            kw = dict(A=np.eye(3)[None] + 0.1 * rng.random((nq, 3, 3)), b=rng.random((nq, 3)),
+                      c=rng.random((nq, 3)), a0=rng.random(nq))
+            kern = P.GeneralKernel(mesh, **kw)
+        plan = DeviceMesh(mesh.q, mesh.me, mesh.vols, core="Haswell").plan(1)
+        (csr,) = plan.assemble([kern])
+        got = to_host(csr)
+        op = O.OracleOp(kind, 3, mesh.vols, core="Haswell", **kw)
+        assert_csr_equal(got, *O.assemble(mesh.q, mesh.me, op, nthreads=4))
