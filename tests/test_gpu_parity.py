@@ -372,3 +372,34 @@ def test_haswell_core_vs_oracle(cuda_ok, kernel, monkeypatch):
         got = to_host(csr)
         op = O.OracleOp(kind, 3, mesh.vols, core="Haswell", **kw)
         assert_csr_equal(got, *O.assemble(mesh.q, mesh.me, op, nthreads=4))
+
+
+@pytest.mark.parametrize("kernel", ["rowgather", "twopass"])
+def test_edge_cases_empty_and_isolated(cuda_ok, kernel, monkeypatch):
+    # reference edge cases: a zero kernel gives an empty matrix
+    # (test_assembly.py:99-102, sparse.py:91-95/108-111); nodes no element
+    # references give empty rows; a mesh without elements; a row block of
+    # isolated nodes only
+    from oracle import oracle as O
+    from paper_1401_3301_b200.device import DeviceMesh
+
+    monkeypatch.setenv("SA_KERNEL", kernel)
+    mesh = _jittered(2, 6, 3)
+    nq = mesh.q.shape[1]
+    z = P.assemble_b200(mesh, P.MassKernel(mesh, np.zeros(nq)))
+    assert z.nnz == 0 and np.array_equal(z.row_ptr, np.zeros(nq + 1, dtype=np.int64))
+    # 5 isolated nodes appended (never referenced)
+    q2 = np.hstack([mesh.q, np.full((2, 5), 0.5)])
+    mesh2 = P.Mesh(q2, mesh.me, mesh.vols)
+    got = P.assemble_b200(mesh2, P.StiffnessKernel(mesh2))
+    rp, ci, va = O.assemble(q2, mesh.me, O.OracleOp("stiffness", 2, mesh.vols), nthreads=2)
+    assert_csr_equal(got, rp, ci, va)
+    assert np.all(np.diff(got.row_ptr)[nq:] == 0)
+    # a row block holding only the isolated nodes
+    (csr,) = DeviceMesh(q2, mesh.me, mesh.vols).plan(1, nq, nq + 5).assemble([P.StiffnessKernel(mesh2)])
+    assert csr.nnz == 0 and csr.indptr.cpu().numpy().tolist() == [0] * 6
+    # no elements at all
+    for d in (1, 2, 3):
+        e = P.Mesh(np.zeros((d, 4)), np.zeros((d + 1, 0), dtype=np.int64), np.zeros(0))
+        m0 = P.assemble_b200(e, P.StiffnessKernel(e))
+        assert m0.nnz == 0 and m0.shape == (4, 4)
