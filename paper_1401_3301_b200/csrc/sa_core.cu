@@ -1351,8 +1351,8 @@ __device__ __forceinline__ void element_from_stage(const double *__restrict__ vr
     }
 }
 
-template <int D, int M, int OPS, int CORE>
-__global__ void __launch_bounds__(EB_SIZE, 4) k_element_rows_batched(NumArgs a)
+template <int D, int M, int OPS, int CORE, int MINB>
+__global__ void __launch_bounds__(EB_SIZE, MINB) k_element_rows_batched(NumArgs a)
 {
     extern __shared__ double vrec[];
     const int t = threadIdx.x;
@@ -2255,7 +2255,11 @@ int launch_twopass(const NumArgs &a, int64_t nnodes, cudaStream_t st)
             // batched element pass (vertex records deduplicated per batch in smem)
             batched = true;
             const size_t smem = (size_t)std::max(a.eb_maxn, 1) * EB_REC * sizeof(double);
-            auto kern = k_element_rows_batched<D, M, OPS, CORE>;
+            // SA_EMINB for the batched pass: 3 | 4 (default) | 5 blocks per SM
+            const int bm = emb_s ? atoi(emb_s) : 4;
+            auto kern = bm == 3 ? k_element_rows_batched<D, M, OPS, CORE, 3>
+                        : bm == 5 ? k_element_rows_batched<D, M, OPS, CORE, 5>
+                                  : k_element_rows_batched<D, M, OPS, CORE, 4>;
             SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             if (a.ne) SA_LAUNCH(kern, grid_for(a.ne, EB_SIZE), EB_SIZE, smem, st, a);
         }
