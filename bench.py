@@ -59,8 +59,7 @@ def profiled_traffic(name):
 
     if os.environ.get("SA_KERNEL") or os.environ.get("SA_BENCH_RENUMBER"):
         return {"traffic": None}
-    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"ncu_{name}_numeric_*.json")),
-                   key=os.path.getmtime)
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"ncu_{name}_numeric_*.json")))  # by round/tag
     if not paths:
         return {"traffic": None}
     try:
