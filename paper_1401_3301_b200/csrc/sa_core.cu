@@ -923,9 +923,17 @@ __device__ __forceinline__ void krow_runtime(const NumArgs &a, const ElemGeo<D> 
 // accumulators indexed by the 8-bit column ranks stored with each incidence.
 // Used when a node has more than 31 incidences or the block kernel's shared
 // memory does not fit.
-template <int D, int M, int OPS, int CORE, int ILP, int MINB, bool PRE = false>
-__global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a)
+template <int D, int M, int OPS, int CORE, int ILP, int MINB, bool PRE = false, bool LEAN = false>
+__global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
 {
+    // LEAN: no diagnostics and a constant mass weight, known at compile time
+    // (the local copy is scalar-replaced; w == nullptr and dbg == 0 fold the
+    // weight loads and the diagnostic branches away)
+    NumArgs a = a_in;
+    if constexpr (LEAN) {
+        a.w = nullptr;
+        a.dbg = 0;
+    }
     constexpr int NOUT = n_outputs<OPS>();
     extern __shared__ double smem_acc[];
     const int tid = threadIdx.x, lane = tid & 31;
@@ -2161,11 +2169,19 @@ int launch_rowgather(const NumArgs &a, int64_t nnodes, cudaStream_t st)
     if (smem > 200 * 1024)
         return set_error(SA_ERR_CAPACITY, "row accumulators need %zu B of shared memory per %d threads", smem, block);
     void (*kern)(NumArgs);
+    // lean instances (SA_LEAN=0 disables) when no diagnostics run and any mass
+    // weight is constant
+    const char *ln_s = getenv("SA_LEAN");
+    const bool lean = (ln_s ? atoi(ln_s) != 0 : true) && a.dbg == 0 && !((OPS & OP_MASS) && a.w);
     if (ilp == 2) kern = k_numeric_rowgather<D, M, OPS, CORE, 2, 1>;
-    else if (ilp == 3) kern = k_numeric_rowgather<D, M, OPS, CORE, 3, 1>;
-    else if (minb == 8) kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 8>;
-    else if (minb == 6) kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 6>;
-    else if (minb == 3) kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 3>;
+    else if (ilp == 3) kern = lean ? k_numeric_rowgather<D, M, OPS, CORE, 3, 1, false, true>
+                                   : k_numeric_rowgather<D, M, OPS, CORE, 3, 1>;
+    else if (minb == 8) kern = lean ? k_numeric_rowgather<D, M, OPS, CORE, 1, 8, false, true>
+                                    : k_numeric_rowgather<D, M, OPS, CORE, 1, 8>;
+    else if (minb == 6) kern = lean ? k_numeric_rowgather<D, M, OPS, CORE, 1, 6, false, true>
+                                    : k_numeric_rowgather<D, M, OPS, CORE, 1, 6>;
+    else if (minb == 3) kern = lean ? k_numeric_rowgather<D, M, OPS, CORE, 1, 3, false, true>
+                                    : k_numeric_rowgather<D, M, OPS, CORE, 1, 3>;
     else kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 1>;
     SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (nnodes) SA_LAUNCH(kern, grid_for(nnodes, block), block, smem, st, a);
