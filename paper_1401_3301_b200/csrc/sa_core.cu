@@ -1009,10 +1009,12 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
             accum(vals, rec.y);
         };
         const int64_t t0 = inc0;
-        const IncRec *wrec = a.winc ? a.winc + a.wseg[nl >> 5] + (nl & 31) : nullptr;
+        // (lean instances: warp-interleaved records exactly in 3D)
+        const bool use_w = LEAN ? D == 3 : a.winc != nullptr;
+        const IncRec *wrec = use_w ? a.winc + a.wseg[nl >> 5] + (nl & 31) : nullptr;
         // stage 1 of incidence t: its record, connectivity and volume
         auto load1 = [&](int64_t t, uint2 &rec, ElemRaw<D> &x) {
-            if (wrec) {
+            if (use_w) {
                 unsigned long long u0, u1, u2, u3;
                 asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];"
                     : "=l"(u0), "=l"(u1), "=l"(u2), "=l"(u3)
@@ -2172,7 +2174,8 @@ int launch_rowgather(const NumArgs &a, int64_t nnodes, cudaStream_t st)
     // lean instances (SA_LEAN=0 disables) when no diagnostics run and any mass
     // weight is constant
     const char *ln_s = getenv("SA_LEAN");
-    const bool lean = (ln_s ? atoi(ln_s) != 0 : true) && a.dbg == 0 && !((OPS & OP_MASS) && a.w);
+    const bool lean = (ln_s ? atoi(ln_s) != 0 : true) && a.dbg == 0 && !((OPS & OP_MASS) && a.w) &&
+                      (a.winc != nullptr) == (D == 3);
     if (ilp == 2) kern = k_numeric_rowgather<D, M, OPS, CORE, 2, 1>;
     else if (ilp == 3) kern = lean ? k_numeric_rowgather<D, M, OPS, CORE, 3, 1, false, true>
                                    : k_numeric_rowgather<D, M, OPS, CORE, 3, 1>;
