@@ -911,6 +911,31 @@ __device__ __forceinline__ void element_krow(const NumArgs &a, const ElemGeo<D> 
     }
 }
 
+// Local row alpha of constant-weight mass and/or stiffness with alpha chosen
+// by selects instead of a branch per alpha: one copy of the arithmetic
+// (G_alpha selected, then element_krow's operations in element_krow's order:
+// the same values bit for bit).  Lean row-gather instances use it.
+template <int D, int OPS>
+__device__ __forceinline__ void element_krow_sel(const NumArgs &a, const ElemGeo<D> &g, int alpha, double *dst)
+{
+    constexpr int NOUT = n_outputs<OPS>();
+    int o = 0;
+    if constexpr ((OPS & OP_MASS) != 0) {
+        const double cd = SA_MUL(a.mass_coef_diag, g.vol), co = SA_MUL(a.mass_coef_off, g.vol);
+        const double vd = SA_MUL(cd, a.mass_wc), vo = SA_MUL(co, a.mass_wc);
+#pragma unroll
+        for (int b = 0; b <= D; ++b) dst[b * NOUT + o] = b == alpha ? vd : vo;
+        ++o;
+    }
+    if constexpr ((OPS & OP_STIFF) != 0) {
+        double ga[D];
+        select_row<D>(g.G, alpha, ga);
+#pragma unroll
+        for (int b = 0; b <= D; ++b) dst[b * NOUT + o] = stiff_entry<D>(ga, g.G[b], g.vol);
+        ++o;
+    }
+}
+
 // runtime local row alpha -> compile-time element_krow<alpha>
 template <int D, int M, int OPS, int A = 0>
 __device__ __forceinline__ void krow_runtime(const NumArgs &a, const ElemGeo<D> &g, int alpha, double *vals)
@@ -1000,7 +1025,10 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
             const int64_t e = rec.x & 0x3fffffffu;
             if (element_compute<D, OPS, CORE>(x, g)) emin = min(emin, e);
             double vals[(D + 1) * NOUT * MM];
-            krow_runtime<D, M, OPS>(a, g, rec.x >> 30, vals);
+            if constexpr (LEAN && M == 1 && (OPS & ~(OP_MASS | OP_STIFF)) == 0)
+                element_krow_sel<D, OPS>(a, g, rec.x >> 30, vals);
+            else
+                krow_runtime<D, M, OPS>(a, g, rec.x >> 30, vals);
             if (a.dbg == 2) {   // diagnostics: no folds
 #pragma unroll
                 for (int i = 0; i < (D + 1) * NOUT * MM; ++i) dsum += vals[i];
