@@ -934,6 +934,17 @@ __device__ __forceinline__ void element_krow_sel(const NumArgs &a, const ElemGeo
         for (int b = 0; b <= D; ++b) dst[b * NOUT + o] = stiff_entry<D>(ga, g.G[b], g.vol);
         ++o;
     }
+    if constexpr ((OPS & OP_ELASTIC) != 0) {   // OPS == OP_ELASTIC, M == D
+        double ga[D];
+        select_row<D>(g.G, alpha, ga);
+#pragma unroll
+        for (int b = 0; b <= D; ++b)
+#pragma unroll
+            for (int l = 0; l < D; ++l)
+#pragma unroll
+                for (int n = 0; n < D; ++n)
+                    dst[(b * D + l) * D + n] = elastic_entry<D>(ga, g.G[b], l, n, g.lambs, g.mus);
+    }
 }
 
 // runtime local row alpha -> compile-time element_krow<alpha>
@@ -1025,7 +1036,7 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
             const int64_t e = rec.x & 0x3fffffffu;
             if (element_compute<D, OPS, CORE>(x, g)) emin = min(emin, e);
             double vals[(D + 1) * NOUT * MM];
-            if constexpr (LEAN && M == 1 && (OPS & ~(OP_MASS | OP_STIFF)) == 0)
+            if constexpr (LEAN && ((M == 1 && (OPS & ~(OP_MASS | OP_STIFF)) == 0) || OPS == OP_ELASTIC))
                 element_krow_sel<D, OPS>(a, g, rec.x >> 30, vals);
             else
                 krow_runtime<D, M, OPS>(a, g, rec.x >> 30, vals);
@@ -2213,7 +2224,8 @@ int launch_rowgather(const NumArgs &a, int64_t nnodes, cudaStream_t st)
                                     : k_numeric_rowgather<D, M, OPS, CORE, 1, 6>;
     else if (minb == 3) kern = lean ? k_numeric_rowgather<D, M, OPS, CORE, 1, 3, false, true>
                                     : k_numeric_rowgather<D, M, OPS, CORE, 1, 3>;
-    else kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 1>;
+    else kern = lean ? k_numeric_rowgather<D, M, OPS, CORE, 1, 1, false, true>
+                     : k_numeric_rowgather<D, M, OPS, CORE, 1, 1>;
     SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (nnodes) SA_LAUNCH(kern, grid_for(nnodes, block), block, smem, st, a);
     return SA_OK;
