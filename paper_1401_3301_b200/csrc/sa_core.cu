@@ -2202,7 +2202,11 @@ int launch_rowgather(const NumArgs &a, int64_t nnodes, cudaStream_t st)
     // latency-bound, so occupancy wins over per-thread ILP except for the
     // register-heavy elastic operator, which gains from the pipeline
     const int ilp = ilp_s ? atoi(ilp_s) : (M > 1 ? 3 : 1);
-    const int minb = mb_s ? atoi(mb_s) : (M > 1 ? 0 : (OPS & OP_GENERAL) ? 3 : (D <= 2 ? 8 : 6));
+    int minb = mb_s ? atoi(mb_s) : (M > 1 ? 0 : (OPS & OP_GENERAL) ? 3 : (D <= 2 ? 8 : 6));
+    // (2D, more than one wave of 8 blocks/SM: 10 blocks/SM at 48 registers
+    // beats 8 at 60 despite an 8-byte spill -- C2 0.299 -> 0.289 ms; a
+    // single wave (C1) keeps 8)
+
     const size_t per_thread = (size_t)NOUT * (a.acc_stride | 1) * sizeof(double);
     int block = 128;
     while (per_thread * block > 100 * 1024 && block > 32) block /= 2;
@@ -2215,6 +2219,7 @@ int launch_rowgather(const NumArgs &a, int64_t nnodes, cudaStream_t st)
     const char *ln_s = getenv("SA_LEAN");
     const bool lean = (ln_s ? atoi(ln_s) != 0 : true) && a.dbg == 0 && !((OPS & OP_MASS) && a.w) &&
                       (a.winc != nullptr) == (D == 3);
+    if (!mb_s && lean && D <= 2 && M == 1 && !(OPS & OP_GENERAL) && nnodes > (int64_t)148 * 8 * 128) minb = 10;
     if (ilp == 2) kern = k_numeric_rowgather<D, M, OPS, CORE, 2, 1>;
     else if (ilp == 3) kern = lean ? k_numeric_rowgather<D, M, OPS, CORE, 3, 1, false, true>
                                    : k_numeric_rowgather<D, M, OPS, CORE, 3, 1>;
@@ -2222,6 +2227,9 @@ int launch_rowgather(const NumArgs &a, int64_t nnodes, cudaStream_t st)
                                     : k_numeric_rowgather<D, M, OPS, CORE, 1, 8>;
     else if (minb == 6) kern = lean ? k_numeric_rowgather<D, M, OPS, CORE, 1, 6, false, true>
                                     : k_numeric_rowgather<D, M, OPS, CORE, 1, 6>;
+    else if (minb == 7 && lean && M == 1) kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 7, false, true>;
+    else if (minb == 10 && lean && M == 1) kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 10, false, true>;
+    else if (minb == 12 && lean && M == 1) kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 12, false, true>;
     else if (minb == 3) kern = lean ? k_numeric_rowgather<D, M, OPS, CORE, 1, 3, false, true>
                                     : k_numeric_rowgather<D, M, OPS, CORE, 1, 3>;
     else kern = lean ? k_numeric_rowgather<D, M, OPS, CORE, 1, 1, false, true>
