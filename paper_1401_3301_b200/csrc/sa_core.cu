@@ -104,6 +104,7 @@ struct sa_plan {
     int32_t *eb_verts = nullptr, *eb_count = nullptr;
     uint32_t *eb_loc = nullptr;
     int eb_maxn = 0;
+    bool eb_allfit = false;        // every batch staged (no direct-gather fallback compiled in)
 };
 
 // numeric-phase arguments (shared by the per-dimension translation units)
@@ -139,6 +140,7 @@ struct NumArgs {
     const int32_t *eb_verts, *eb_count;
     const uint32_t *eb_loc;
     int eb_maxn;
+    int eb_allfit;
     double mass_coef_diag, mass_coef_off;  // 2/((d+1)(d+2)(d+3)), 1/(...) as Python computes them
     double mass_wc;  // constant weight: (wsum + w) + w, the same for every (alpha, beta)
 };
@@ -1361,7 +1363,7 @@ __global__ void __launch_bounds__(EB_SIZE) k_eb_build(const typename IdxT<D>::ty
     __syncthreads();
     if (t == 0) {
         count[b] = n <= EB_CAP ? n : -1;
-        if (n <= EB_CAP) atomicMax(maxn, (unsigned long long)n);
+        atomicMax(maxn, (unsigned long long)n);   // > EB_CAP: some batch takes the direct path
     }
     if (i < ne && n <= EB_CAP) {
         unsigned l = 0;
@@ -1400,7 +1402,7 @@ __device__ __forceinline__ void element_from_stage(const double *__restrict__ vr
     }
 }
 
-template <int D, int M, int OPS, int CORE, int MINB>
+template <int D, int M, int OPS, int CORE, int MINB, bool ALLFIT = false>
 __global__ void __launch_bounds__(EB_SIZE, MINB) k_element_rows_batched(NumArgs a)
 {
     extern __shared__ double vrec[];
@@ -1408,7 +1410,8 @@ __global__ void __launch_bounds__(EB_SIZE, MINB) k_element_rows_batched(NumArgs 
     const int64_t b = blockIdx.x, i = b * EB_SIZE + t;
     const bool in = i < a.ne;
     const int64_t e = a.e_lo + i;
-    const int n = __ldg(a.eb_count + b);
+    // ALLFIT: every batch is staged (the direct-gather fallback is not compiled)
+    const int n = ALLFIT ? max(__ldg(a.eb_count + b), 0) : __ldg(a.eb_count + b);
     uint4 p = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
     unsigned lc = 0;
     ElemRaw<D> x;
@@ -2326,7 +2329,8 @@ int launch_twopass(const NumArgs &a, int64_t nnodes, cudaStream_t st)
             const int bm = emb_s ? atoi(emb_s) : 4;
             auto kern = bm == 3 ? k_element_rows_batched<D, M, OPS, CORE, 3>
                         : bm == 5 ? k_element_rows_batched<D, M, OPS, CORE, 5>
-                                  : k_element_rows_batched<D, M, OPS, CORE, 4>;
+                        : a.eb_allfit ? k_element_rows_batched<D, M, OPS, CORE, 4, true>
+                                      : k_element_rows_batched<D, M, OPS, CORE, 4>;
             SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             if (a.ne) SA_LAUNCH(kern, grid_for(a.ne, EB_SIZE), EB_SIZE, smem, st, a);
         }
@@ -2672,7 +2676,8 @@ static int ensure_twopass(sa_plan *P, int kstride, bool batches, cudaStream_t st
         SA_CUDA_TRY(cudaMemcpyAsync(&h, mx, sizeof h, cudaMemcpyDeviceToHost, st));
         SA_CUDA_TRY(cudaStreamSynchronize(st));
         SA_CUDA_TRY(cudaFreeAsync(mx, st));
-        P->eb_maxn = (int)h;
+        P->eb_maxn = (int)std::min<unsigned long long>(h, EB_CAP);
+        P->eb_allfit = h <= EB_CAP;
     }
     const int64_t kelems = (int64_t)kstride * P->tp_nslots;
     if (P->kbuf_elems < kelems) {
@@ -2760,6 +2765,7 @@ int sa_numeric(sa_plan *P, int ops, const sa_coeffs *cf, double *const *vals_dev
             a.eb_count = P->eb_count;
             a.eb_loc = P->eb_loc;
             a.eb_maxn = P->eb_maxn;
+            a.eb_allfit = P->eb_allfit ? 1 : 0;
         }
         a.kbuf = P->kbuf;
         a.kstride = ks;
