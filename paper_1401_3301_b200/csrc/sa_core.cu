@@ -1450,6 +1450,111 @@ __global__ void __launch_bounds__(EB_SIZE, MINB) k_element_rows_batched(NumArgs 
     element_rows_store<D, M, OPS>(a, g, pos);
 }
 
+// Pipelined batched element pass (every batch staged): persistent blocks
+// walk batches b, b + G, b + 2G, ... with a three-stage cp.async pipeline --
+// the vertex list of batch k+2 and the vertex records of batch k+1 are in
+// flight while batch k is computed -- so the staging latency hides behind
+// the fp64 work instead of alternating with it.  Same per-element values.
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int D, int M, int OPS, int CORE, int MINB>
+__global__ void __launch_bounds__(EB_SIZE, MINB) k_element_rows_pipe(NumArgs a)
+{
+    extern __shared__ double dyn[];
+    double *recs = dyn;                                                 // [2][maxn][EB_REC]
+    int *svs = (int *)(dyn + 2 * (size_t)a.eb_maxn * EB_REC);           // [3][EB_CAP + 1] (+ count)
+    const int t = threadIdx.x;
+    const int64_t nb = (a.ne + EB_SIZE - 1) / EB_SIZE;
+    const int64_t G = gridDim.x;
+    const int RS = a.eb_maxn * EB_REC;
+    auto issue_list = [&](int64_t bb, int stage) {   // vertex list + count of batch bb
+        if (bb >= nb) return;
+        int *sv = svs + stage * (EB_CAP + 1);
+        const int32_t *vl = a.eb_verts + bb * EB_CAP;
+        for (int s = t; s < EB_CAP; s += EB_SIZE) cp_async4(sv + s, vl + s);
+        if (t == 0) cp_async4(sv + EB_CAP, a.eb_count + bb);
+    };
+    auto issue_recs = [&](int64_t bb, int lstage, int rstage) {   // vertex records of batch bb
+        if (bb >= nb) return;
+        const int *sv = svs + lstage * (EB_CAP + 1);
+        double *rec = recs + (size_t)rstage * RS;
+        const int n = sv[EB_CAP];
+        for (int c = t; c < n * 10; c += EB_SIZE) {
+            const int s = c / 10, h = c - 10 * s;
+            const int64_t vv = sv[s];
+            const double *src = h < 2 ? (const double *)a.qv + vv * 4 + 2 * h : a.gen_packed + vv * 16 + 2 * (h - 2);
+            cp_async16(rec + s * EB_REC + 2 * h, src);
+        }
+    };
+    const int64_t b0 = blockIdx.x;
+    if (b0 >= nb) return;
+    // prologue: lists of batches 0 and 1, then records of batch 0
+    issue_list(b0, 0);
+    cp_async_commit();
+    issue_list(b0 + G, 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    issue_recs(b0, 0, 0);
+    cp_async_commit();
+    // this thread's element data of the current batch (registers, one ahead)
+    auto own = [&](int64_t bb, uint4 &p, unsigned &lc, double &vol) {
+        const int64_t i = bb * EB_SIZE + t;
+        p = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+        lc = 0;
+        vol = 0.0;
+        if (bb < nb && i < a.ne) {
+            p = __ldg(a.epos + i);
+            lc = __ldg(a.eb_loc + i);
+            vol = __ldg(a.vols + a.e_lo + i);
+        }
+    };
+    uint4 p;
+    unsigned lc;
+    double vol;
+    own(b0, p, lc, vol);
+    for (int64_t k = 0;; ++k) {
+        const int64_t b = b0 + k * G;
+        if (b >= nb) break;
+        issue_list(b + 2 * G, (int)((k + 2) % 3));
+        cp_async_commit();
+        cp_async_wait<1>();   // records of batch k and the list of batch k+1 have landed
+        __syncthreads();
+        issue_recs(b + G, (int)((k + 1) % 3), (int)((k + 1) & 1));
+        cp_async_commit();
+        uint4 pn;
+        unsigned lcn;
+        double voln;
+        own(b + G, pn, lcn, voln);
+        const int64_t i = b * EB_SIZE + t;
+        const unsigned pos[4] = {p.x, p.y, p.z, p.w};
+        bool any = false;
+#pragma unroll
+        for (int kk = 0; kk <= D; ++kk) any |= pos[kk] != 0xffffffffu;
+        if (i < a.ne && any) {
+            ElemRaw<D> x;
+            x.vol = vol;
+            element_from_stage<D, OPS>(recs + (size_t)(k & 1) * RS, lc, x);
+            ElemGeo<D> g;
+            if (element_compute<D, OPS, CORE>(x, g))
+                atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)(a.e_lo + i));
+            element_rows_store<D, M, OPS>(a, g, pos);
+        }
+        p = pn;
+        lc = lcn;
+        vol = voln;
+        __syncthreads();   // stage k & 1 is rewritten by the records of batch k+2
+    }
+    cp_async_wait<0>();
+}
+
 // element range of the block's incidences: out[0] = min e, out[1] = max e
 __global__ void k_inc_erange(const uint2 *__restrict__ inc, int64_t n, unsigned long long *out)
 {
@@ -2327,12 +2432,32 @@ int launch_twopass(const NumArgs &a, int64_t nnodes, cudaStream_t st)
             const size_t smem = (size_t)std::max(a.eb_maxn, 1) * EB_REC * sizeof(double);
             // SA_EMINB for the batched pass: 3 | 4 (default) | 5 blocks per SM
             const int bm = emb_s ? atoi(emb_s) : 4;
-            auto kern = bm == 3 ? k_element_rows_batched<D, M, OPS, CORE, 3>
-                        : bm == 5 ? k_element_rows_batched<D, M, OPS, CORE, 5>
-                        : a.eb_allfit ? k_element_rows_batched<D, M, OPS, CORE, 4, true>
-                                      : k_element_rows_batched<D, M, OPS, CORE, 4>;
-            SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            if (a.ne) SA_LAUNCH(kern, grid_for(a.ne, EB_SIZE), EB_SIZE, smem, st, a);
+            const char *pp_s = getenv("SA_EPIPE");
+            const bool pipe = a.eb_allfit && (pp_s ? atoi(pp_s) != 0 : true);
+            if (pipe) {
+                // persistent, three-stage cp.async pipeline
+                // (C5: 3 blocks/SM at 164 registers 6.73 ms, 4 at 128 + spill 6.79,
+                // unpipelined batched 7.18)
+                const int pm = pp_s && atoi(pp_s) > 1 ? atoi(pp_s) : 3;
+                auto pk = pm == 3 ? k_element_rows_pipe<D, M, OPS, CORE, 3> : k_element_rows_pipe<D, M, OPS, CORE, 4>;
+                const size_t psm = 2 * (size_t)std::max(a.eb_maxn, 1) * EB_REC * sizeof(double) +
+                                   3 * (EB_CAP + 1) * sizeof(int);
+                SA_CUDA_TRY(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+                int dev = 0, nsm = 148, occ = 0;
+                SA_CUDA_TRY(cudaGetDevice(&dev));
+                SA_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+                SA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pk, EB_SIZE, psm));
+                const int64_t nb = (a.ne + EB_SIZE - 1) / EB_SIZE;
+                const unsigned g = (unsigned)std::min<int64_t>(nb, (int64_t)nsm * std::max(occ, 1));
+                if (a.ne) SA_LAUNCH(pk, g, EB_SIZE, psm, st, a);
+            } else {
+                auto kern = bm == 3 ? k_element_rows_batched<D, M, OPS, CORE, 3>
+                            : bm == 5 ? k_element_rows_batched<D, M, OPS, CORE, 5>
+                            : a.eb_allfit ? k_element_rows_batched<D, M, OPS, CORE, 4, true>
+                                          : k_element_rows_batched<D, M, OPS, CORE, 4>;
+                SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                if (a.ne) SA_LAUNCH(kern, grid_for(a.ne, EB_SIZE), EB_SIZE, smem, st, a);
+            }
         }
     }
     if (batched) {
