@@ -140,7 +140,7 @@ def numeric_kernels(cfg):
     if k == "chunk":
         return "k_numeric_chunks"
     if k == "twopass" or (not k and cfg["d"] == 3 and cfg["ops"] == ("general",)):
-        return "k_element_rows_batched + k_numeric_rowgather<PRE> (two-pass; time = both)"
+        return "k_element_rows_pipe + k_numeric_rowgather<PRE> (two-pass; time = both)"
     return "k_numeric_rowgather"
 
 

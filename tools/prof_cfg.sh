@@ -8,7 +8,7 @@ cd "${GRAFT_REPO_ROOT:-$(dirname $0)/..}"
 mkdir -p gpurun_out
 TAG=${TAG:-r01}
 CFG=${CFG:-C2}
-case $CFG in C5) KS=${KERNELS:-"k_element_rows_batched k_numeric_rowgather"};; *) KS=${KERNELS:-k_numeric_rowgather};; esac
+case $CFG in C5) KS=${KERNELS:-"k_element_rows_pipe k_numeric_rowgather"};; *) KS=${KERNELS:-k_numeric_rowgather};; esac
 CMD="python bench.py --config $CFG --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/plain_${CFG}_${TAG}.log 2>&1 || { echo "plain run failed"; exit 1; }
 FILES=""
