@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -309,16 +310,19 @@ def main():
     d = cfg["d"]
     n_g = cfg["n"] if (world == 1 or args.scaling == "strong") else int(round(cfg["n"] * world ** (1.0 / d)))
     gcfg = dict(cfg, n=n_g)
-    q, me = make_mesh(gcfg)
-    nq, nme = q.shape[1], me.shape[1]
     m = d if "elastic" in cfg["ops"] else 1
-    rb, re_ = parallel.row_blocks(nq, m, world)[rank]
     if world > 1:
-        sl = parallel.slab(q, me, m, rb, re_)
+        # the rank's slab generated on its own B200 (no global mesh anywhere)
+        nq, nme = (n_g + 1) ** d, math.factorial(d) * n_g ** d
+        rb, re_ = parallel.row_blocks(nq, m, world)[rank]
+        sl = P.device_hypercube_slab(d, n_g, m, rb, re_, seed=gcfg["seed"], amplitude=0.2 if d == 2 else 0.15,
+                                     device=dev)
         q_r, me_r, col_off, lo = sl.q, sl.me, sl.col_offset, sl.node_lo
         rb_r, re_r = sl.row_begin, sl.row_end
-        del q, me
     else:
+        q, me = make_mesh(gcfg)
+        nq, nme = q.shape[1], me.shape[1]
+        rb, re_ = parallel.row_blocks(nq, m, world)[rank]
         q_r, me_r, col_off, lo, rb_r, re_r = q, me, 0, 0, rb, re_
     vols = P.device_volumes(q_r, me_r)
     mesh = P.Mesh(q_r, me_r, vols)

@@ -180,6 +180,13 @@ int sa_pk_plan_destroy(sa_pk_plan *plan);
  * Either buffer may be NULL. */
 int sa_kuhn_mesh(int d, int64_t n, int jitter, double lo, double range, uint64_t state_hi, uint64_t state_lo,
                  uint64_t inc_hi, uint64_t inc_lo, double *q_dev, int64_t *me_dev, void *stream);
+/* The window of that mesh a rank needs: nodes [v0, v1) -> q_dev (d, v1-v0)
+ * (jitter by PCG64 jump-ahead to each node's draws) and elements [e0, e1) ->
+ * me_dev (d+1, e1-e0) with node ids relative to v0; bitwise the
+ * corresponding slices of sa_kuhn_mesh's arrays. */
+int sa_kuhn_slab(int d, int64_t n, int jitter, double lo, double range, uint64_t state_hi, uint64_t state_lo,
+                 uint64_t inc_hi, uint64_t inc_lo, int64_t v0, int64_t v1, int64_t e0, int64_t e1, double *q_dev,
+                 int64_t *me_dev, void *stream);
 
 #ifdef __cplusplus
 }

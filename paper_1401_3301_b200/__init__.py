@@ -20,6 +20,7 @@ from .kernels import ElasticKernel, GeneralKernel, MassKernel, StiffnessKernel
 from .mesh import (
     Mesh,
     device_hypercube_arrays,
+    device_hypercube_slab,
     generate_hypercube_mesh,
     hypercube_arrays,
     jitter_interior,

@@ -25,7 +25,7 @@ SA_CORE = {"SkylakeX": 0, "Haswell": 1}
 EXPORTS = (
     "sa_mesh_create", "sa_mesh_vols", "sa_mesh_destroy",
     "sa_plan_create", "sa_plan_info", "sa_plan_stats", "sa_plan_pattern", "sa_plan_destroy",
-    "sa_numeric", "sa_compact", "sa_plan_prepare", "sa_mesh_set_coords", "sa_kuhn_mesh",
+    "sa_numeric", "sa_compact", "sa_plan_prepare", "sa_mesh_set_coords", "sa_kuhn_mesh", "sa_kuhn_slab",
     "sa_pk_plan_create", "sa_pk_plan_info", "sa_pk_plan_pattern", "sa_pk_mass", "sa_pk_compact", "sa_pk_plan_destroy",
     "sa_last_error", "sa_bad_index", "sa_launch_count",
 )
@@ -89,6 +89,8 @@ def load(build_if_missing: bool = True):
     u64 = ctypes.c_uint64
     L.sa_kuhn_mesh.argtypes = [ctypes.c_int, i64, ctypes.c_int, ctypes.c_double, ctypes.c_double, u64, u64, u64, u64,
                                vp, vp, vp]
+    L.sa_kuhn_slab.argtypes = [ctypes.c_int, i64, ctypes.c_int, ctypes.c_double, ctypes.c_double, u64, u64, u64, u64,
+                               i64, i64, i64, i64, vp, vp, vp]
     L.sa_compact.argtypes = [vp, vp, vp, vp, vp, vp]
     L.sa_last_error.restype = ctypes.c_char_p
     L.sa_bad_index.restype = ctypes.c_int64

@@ -110,7 +110,102 @@ __global__ void k_kuhn_me(int d, int dfact, int64_t n, int64_t nme, int64_t *__r
     }
 }
 
+// A node window [v0, v0 + nv) with its jitter (each interior node's d
+// draws by jump-ahead: draw k = axis * n_interior + interior index) and an
+// element window [e0, e0 + ne) with node ids relative to v0: a rank's slab
+// without the global mesh.
+__global__ void k_kuhn_q_range(int d, int64_t n, int64_t v0, int64_t nv, int64_t nint, int jitter, double lo,
+                               double range, uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uint64_t i_lo,
+                               double *__restrict__ q)
+{
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= nv) return;
+    const int64_t v = v0 + t;
+    int64_t idx[3], r = v;
+    bool interior = true;
+    for (int a = d - 1; a >= 0; --a) {
+        idx[a] = r % (n + 1);
+        r /= n + 1;
+        interior &= idx[a] >= 1 && idx[a] <= n - 1;
+    }
+    int64_t j = 0;
+    for (int a = 0; a < d; ++a) j = j * (n - 1) + (idx[a] - 1);
+    const u128 s0 = ((u128)s_hi << 64) | s_lo, inc = ((u128)i_hi << 64) | i_lo;
+    for (int a = 0; a < d; ++a) {
+        double x = __ddiv_rn((double)idx[a], (double)n);
+        if (jitter && interior) {
+            const u128 s = pcg_advance(s0, (uint64_t)(a * nint + j) + 1, inc);
+            const double u = (double)(pcg_output(s) >> 11) * (1.0 / 9007199254740992.0);
+            x = __dadd_rn(x, __dadd_rn(lo, __dmul_rn(range, u)));
+        }
+        q[a * nv + t] = x;
+    }
+}
+
+__global__ void k_kuhn_me_range(int d, int dfact, int64_t n, int64_t e0, int64_t ne, int64_t v0,
+                                int64_t *__restrict__ me)
+{
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= ne) return;
+    const int64_t e = e0 + t;
+    const int64_t cell = e / dfact;
+    const int p = (int)(e - cell * dfact);
+    int64_t stride[3], base = 0, r = cell, s = 1;
+    for (int a = d - 1; a >= 0; --a) {
+        stride[a] = s;
+        base += (r % n) * s;
+        r /= n;
+        s *= n + 1;
+    }
+    int64_t v = base;
+    me[t] = v - v0;
+    for (int j = 0; j < d; ++j) {
+        v += stride[c_perm[p][j]];
+        me[(int64_t)(j + 1) * ne + t] = v - v0;
+    }
+}
+
 }  // namespace
+
+static void kuhn_perms(int d, int (&perm)[6][3])
+{
+    int cur[3] = {0, 1, 2}, k = 0, dfact = 1;
+    for (int a = 2; a <= d; ++a) dfact *= a;
+    do {
+        for (int j = 0; j < d; ++j) perm[k][j] = cur[j];
+        ++k;
+        int i = d - 2;
+        while (i >= 0 && cur[i] > cur[i + 1]) --i;
+        if (i < 0) break;
+        int j = d - 1;
+        while (cur[j] < cur[i]) --j;
+        int t = cur[i]; cur[i] = cur[j]; cur[j] = t;
+        for (int a = i + 1, b = d - 1; a < b; ++a, --b) { t = cur[a]; cur[a] = cur[b]; cur[b] = t; }
+    } while (k < dfact);
+}
+
+extern "C" int sa_kuhn_slab(int d, int64_t n, int jitter, double lo, double range, uint64_t state_hi,
+                            uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t v0, int64_t v1, int64_t e0,
+                            int64_t e1, double *q_dev, int64_t *me_dev, void *stream)
+{
+    if (d < 1 || d > 3) return set_error(SA_ERR_ARG, "dimension must be 1, 2 or 3, got %d", d);
+    if (n < 1) return set_error(SA_ERR_ARG, "subdivision count must be >= 1, got %lld", (long long)n);
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t nq = 1, ncell = 1, nint = 1;
+    int dfact = 1;
+    for (int a = 0; a < d; ++a) { nq *= n + 1; ncell *= n; nint *= n - 1; dfact *= a + 1; }
+    if (v0 < 0 || v1 > nq || v0 > v1 || e0 < 0 || e1 > ncell * dfact || e0 > e1)
+        return set_error(SA_ERR_ARG, "slab window out of range");
+    int perm[6][3] = {{0}};
+    kuhn_perms(d, perm);
+    SA_CUDA_TRY(cudaMemcpyToSymbolAsync(c_perm, perm, sizeof perm, 0, cudaMemcpyHostToDevice, st));
+    if (q_dev && v1 > v0)
+        SA_LAUNCH(k_kuhn_q_range, grid_for(v1 - v0, 128), 128, 0, st, d, n, v0, v1 - v0, nint, jitter && n >= 2, lo,
+                  range, state_hi, state_lo, inc_hi, inc_lo, q_dev);
+    if (me_dev && e1 > e0)
+        SA_LAUNCH(k_kuhn_me_range, grid_for(e1 - e0, 256), 256, 0, st, d, dfact, n, e0, e1 - e0, v0, me_dev);
+    return SA_OK;
+}
 
 extern "C" int sa_kuhn_mesh(int d, int64_t n, int jitter, double lo, double range, uint64_t state_hi,
                             uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, double *q_dev, int64_t *me_dev,

@@ -150,3 +150,53 @@ def device_hypercube_arrays(d: int, n: int, seed: int | None = None, amplitude: 
     if host:
         return q.cpu().numpy(), me.cpu().numpy()
     return q, me
+
+
+def device_hypercube_slab(d: int, n: int, m: int, row_begin: int, row_end: int, seed: int | None = None,
+                          amplitude: float | None = None, device=None):
+    """A rank's slab of the (jittered) Kuhn mesh generated directly on the
+    B200 (sa_kuhn_slab), without the global mesh: the node planes around
+    dof rows [row_begin, row_end) and the cells between them (first
+    coordinate slowest, mesh.py:123-139), node ids relative to the window.
+    A superset of parallel.slab's elements in the same (ascending) order --
+    elements that touch no row of the block contribute nothing to it -- so
+    the block assembles bitwise the rows of the full mesh.  Returns a
+    parallel.Slab with host arrays (vols None: computed by the device mesh)."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .device import _require_cuda, _stream_ptr
+    from .parallel import Slab
+
+    dev = _require_cuda(device)
+    nb0, nb1 = row_begin // m, row_end // m
+    P, C, dfact = (n + 1) ** (d - 1), n ** (d - 1), math.factorial(d)
+    if nb1 > nb0:
+        i0, i1 = nb0 // P, (nb1 - 1) // P
+        c_lo, c_hi = max(i0 - 1, 0), min(i1, n - 1)
+        v0, v1 = max(i0 - 1, 0) * P, (min(i1 + 1, n) + 1) * P
+        e0, e1 = c_lo * C * dfact, (c_hi + 1) * C * dfact
+    else:
+        v0 = v1 = nb0
+        e0 = e1 = 0
+    q = torch.empty((d, v1 - v0), dtype=torch.float64, device=dev)
+    me = torch.empty((d + 1, e1 - e0), dtype=torch.int64, device=dev)
+    lo = rg = 0.0
+    s_hi = s_lo = i_hi = i_lo = 0
+    if seed is not None:
+        if amplitude is None:
+            amplitude = 0.2 if d <= 2 else 0.15
+        h = 1.0 / n
+        lo, hi = -amplitude * h, amplitude * h
+        rg = hi - lo
+        st = np.random.PCG64(seed).state["state"]
+        s_hi, s_lo = st["state"] >> 64, st["state"] & ((1 << 64) - 1)
+        i_hi, i_lo = st["inc"] >> 64, st["inc"] & ((1 << 64) - 1)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.load().sa_kuhn_slab(d, n, 1 if seed is not None else 0, lo, rg, s_hi, s_lo, i_hi, i_lo,
+                                            v0, v1, e0, e1, ctypes.c_void_p(q.data_ptr()),
+                                            ctypes.c_void_p(me.data_ptr()), _stream_ptr()))
+    return Slab(q=q.cpu().numpy(), me=me.cpu().numpy(), vols=None, node_lo=v0, row_begin=m * (nb0 - v0),
+                row_end=m * (nb1 - v0), col_offset=m * v0, elements=np.arange(e0, e1))

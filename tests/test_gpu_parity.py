@@ -403,3 +403,33 @@ def test_edge_cases_empty_and_isolated(cuda_ok, kernel, monkeypatch):
         e = P.Mesh(np.zeros((d, 4)), np.zeros((d + 1, 0), dtype=np.int64), np.zeros(0))
         m0 = P.assemble_b200(e, P.StiffnessKernel(e))
         assert m0.nnz == 0 and m0.shape == (4, 4)
+
+
+@pytest.mark.parametrize("d,n,parts", [(1, 30, 3), (2, 13, 4), (3, 7, 3)])
+def test_device_slab_generator(cuda_ok, d, n, parts):
+    # sa_kuhn_slab windows are bitwise slices of the full generated mesh,
+    # cover every element touching the block, and the blocks assembled from
+    # them stitch to the full oracle matrix
+    from oracle import oracle as O
+    from paper_1401_3301_b200 import parallel
+    from paper_1401_3301_b200.device import DeviceMesh
+
+    seed = 99
+    q, me = P.device_hypercube_arrays(d, n, seed=seed, host=True)
+    nq = q.shape[1]
+    vols = O.volumes(q, me)
+    blocks = []
+    for rb, re_ in parallel.row_blocks(nq, 1, parts):
+        sl = P.device_hypercube_slab(d, n, 1, rb, re_, seed=seed)
+        e = sl.elements
+        assert np.array_equal(sl.q.view(np.int64), q[:, sl.node_lo:sl.node_lo + sl.q.shape[1]].view(np.int64))
+        assert np.array_equal(sl.me + sl.node_lo, me[:, e])
+        touching = parallel.slab(q, me, 1, rb, re_).elements
+        assert np.all(np.isin(touching, e))
+        (csr,) = DeviceMesh(sl.q, sl.me, vols[e]).plan(1, sl.row_begin, sl.row_end).assemble(
+            [P.StiffnessKernel(P.Mesh(sl.q, sl.me, vols[e]))])
+        blocks.append((rb, re_, csr.indptr.cpu().numpy(), csr.indices.cpu().numpy().astype(np.int64) + sl.col_offset,
+                       csr.vals.cpu().numpy()))
+    rp, ci, va = parallel.stitch(blocks, nq, nq)
+    assert_csr_equal(P.SparseMatrix(nq, nq, rp, ci, va),
+                     *O.assemble(q, me, O.OracleOp("stiffness", d, vols), nthreads=4))
