@@ -490,18 +490,21 @@ def run_e2e(q, me, vols, kernels, rb, re_, col_offset, nme_global, args, world, 
     pv = torch.from_numpy(np.asarray(vols)).pin_memory()
     mesh = P.Mesh(pq.numpy(), pme.numpy(), pv.numpy())
     h2d = pq.numel() * 8 + pme.numel() * 8 + pv.numel() * 8
-    steps = max(2, min(args.steps, 5))
+    # two untimed calls (pinned staging buffers and pool memory are set up on
+    # first use), then the median of up to 7 timed calls
+    steps = max(3, min(args.steps, 7))
+    warm = 2
     times = []
     d2h = 0
     stages = {}
-    for i in range(steps + 1):
+    for i in range(steps + warm):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        blocks = assemble_block_b200(mesh, kernels, rb, re_, timings=stages if i > 0 else None,
+        blocks = assemble_block_b200(mesh, kernels, rb, re_, timings=stages if i >= warm else None,
                                      col_offset=col_offset)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        if i > 0:
+        if i >= warm:
             times.append(dt)
         seen, d2h = set(), 0
         for b in blocks:   # shared pattern arrays cross PCIe once; indices as int32
