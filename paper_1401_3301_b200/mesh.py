@@ -152,6 +152,20 @@ def device_hypercube_arrays(d: int, n: int, seed: int | None = None, amplitude: 
     return q, me
 
 
+def kuhn_slab_window(d: int, n: int, nb0: int, nb1: int) -> tuple[int, int, int, int]:
+    """Node window [v0, v1) and element window [e0, e1) of the Kuhn mesh
+    (mesh.py:104-140: nodes row-major with the first coordinate slowest,
+    cells likewise, d! simplices per cell) that hold every element touching
+    nodes [nb0, nb1): the node planes i0-1 .. i1+1 around the block and the
+    cells between them."""
+    P, C, dfact = (n + 1) ** (d - 1), n ** (d - 1), math.factorial(d)
+    if nb1 <= nb0:
+        return nb0, nb0, 0, 0
+    i0, i1 = nb0 // P, (nb1 - 1) // P
+    c_lo, c_hi = max(i0 - 1, 0), min(i1, n - 1)
+    return max(i0 - 1, 0) * P, (min(i1 + 1, n) + 1) * P, c_lo * C * dfact, (c_hi + 1) * C * dfact
+
+
 def device_hypercube_slab(d: int, n: int, m: int, row_begin: int, row_end: int, seed: int | None = None,
                           amplitude: float | None = None, device=None):
     """A rank's slab of the (jittered) Kuhn mesh generated directly on the
@@ -172,15 +186,7 @@ def device_hypercube_slab(d: int, n: int, m: int, row_begin: int, row_end: int, 
 
     dev = _require_cuda(device)
     nb0, nb1 = row_begin // m, row_end // m
-    P, C, dfact = (n + 1) ** (d - 1), n ** (d - 1), math.factorial(d)
-    if nb1 > nb0:
-        i0, i1 = nb0 // P, (nb1 - 1) // P
-        c_lo, c_hi = max(i0 - 1, 0), min(i1, n - 1)
-        v0, v1 = max(i0 - 1, 0) * P, (min(i1 + 1, n) + 1) * P
-        e0, e1 = c_lo * C * dfact, (c_hi + 1) * C * dfact
-    else:
-        v0 = v1 = nb0
-        e0 = e1 = 0
+    v0, v1, e0, e1 = kuhn_slab_window(d, n, nb0, nb1)
     q = torch.empty((d, v1 - v0), dtype=torch.float64, device=dev)
     me = torch.empty((d + 1, e1 - e0), dtype=torch.int64, device=dev)
     lo = rg = 0.0

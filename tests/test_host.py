@@ -144,3 +144,20 @@ def test_slabs_reproduce_full_rows_bitwise():
             blocks.append((rb, re_, ip, ix + sl.col_offset, vv))
         r2, c2, v2 = parallel.stitch(blocks, nq, nq)
         assert np.array_equal(r2, rp) and np.array_equal(c2, ci) and np.array_equal(v2, va)
+
+
+@pytest.mark.parametrize("d,n,parts", [(1, 17, 4), (2, 9, 5), (2, 6, 1), (3, 5, 3), (3, 4, 7)])
+def test_kuhn_slab_window_covers_touching_elements(d, n, parts):
+    # the analytic window device_hypercube_slab generates holds every element
+    # that touches the block's nodes, and every node those elements use
+    from paper_1401_3301_b200 import mesh as M
+    from paper_1401_3301_b200 import parallel
+
+    q, me = P.hypercube_arrays(d, n)
+    for rb, re_ in parallel.row_blocks(q.shape[1], 1, parts):
+        v0, v1, e0, e1 = M.kuhn_slab_window(d, n, rb, re_)
+        touching = parallel.slab(q, me, 1, rb, re_).elements
+        assert np.all((touching >= e0) & (touching < e1))
+        used = me[:, e0:e1]
+        assert used.size == 0 or (used.min() >= v0 and used.max() < v1)
+        assert v0 <= rb and (re_ <= v1 or re_ == rb)
