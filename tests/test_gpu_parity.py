@@ -433,3 +433,31 @@ def test_device_slab_generator(cuda_ok, d, n, parts):
     rp, ci, va = parallel.stitch(blocks, nq, nq)
     assert_csr_equal(P.SparseMatrix(nq, nq, rp, ci, va),
                      *O.assemble(q, me, O.OracleOp("stiffness", d, vols), nthreads=4))
+
+
+def test_general_overlapped_chunks_bitwise(cuda_ok, monkeypatch):
+    # opt-in overlap (element chunks on one stream, folds of finished row
+    # segments on a second) gives the same bits, also under graph replay
+    import torch
+
+    from paper_1401_3301_b200.device import DeviceMesh
+
+    monkeypatch.setenv("SA_OVERLAP", "4")
+    mesh = _jittered(3, 14, 8)
+    nq = mesh.q.shape[1]
+    rng = np.random.default_rng(8)
+    R = rng.standard_normal((nq, 3, 3))
+    f = dict(A=np.eye(3)[None] + 0.5 * np.einsum("nij,nkj->nik", R, R) / 3.0, b=rng.standard_normal((nq, 3)),
+             c=rng.standard_normal((nq, 3)), a0=rng.uniform(0, 1, nq))
+    got = P.assemble_b200(mesh, P.GeneralKernel(mesh, **f))
+    assert_csr_equal(got, *_oracle(mesh, "general", **f))
+    k = [P.GeneralKernel(mesh, **f)]
+    plan = DeviceMesh(mesh.q, mesh.me, mesh.vols).plan(1)
+    ref, _ = plan.numeric(k)
+    ref = ref[0].clone()
+    out = [torch.full((plan.nnz,), float("nan"), dtype=torch.float64, device="cuda")]
+    g = plan.numeric_graph(k, out, plan.resident_coeffs(k))
+    out[0].fill_(float("nan"))
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out[0], ref)
