@@ -50,7 +50,7 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def profiled_traffic(name):
+def profiled_traffic(name, kernel_prefix, world=1):
     """DRAM bytes (read + write) of one numeric step of this config (every
     kernel of the phase), from the newest committed ncu --set full summary
     (profiles/rNN/ncu_<config>_numeric_*.json, tools/prof_cfg.sh +
@@ -58,7 +58,7 @@ def profiled_traffic(name):
     kernels."""
     import glob
 
-    if os.environ.get("SA_KERNEL") or os.environ.get("SA_BENCH_RENUMBER"):
+    if world > 1 or os.environ.get("SA_TUNE") or os.environ.get("SA_BENCH_RENUMBER"):
         return {"traffic": None}
     paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"ncu_{name}_numeric_*.json")))  # by round/tag
     if not paths:
@@ -66,6 +66,8 @@ def profiled_traffic(name):
     try:
         with open(paths[-1]) as f:
             d = json.load(f)
+        if not any(kernel_prefix in k["kernel"] for k in d["kernels"]):
+            return {"traffic": None, "traffic_note": f"no committed ncu capture of {kernel_prefix} for {name}"}
         return {"traffic": float(d["dram_bytes"]), "traffic_source": os.path.relpath(paths[-1], ROOT),
                 "traffic_kernel_ms": float(d["duration_ns"]) * 1e-6,
                 "traffic_kernels": [k["kernel"].split("(")[0].replace("void ", "") for k in d["kernels"]]}
@@ -135,13 +137,12 @@ def make_kernels(cfg, mesh, window=None):
 def numeric_kernels(cfg):
     """The kernel(s) of one numeric step (the default selection in
     sa_core.cu: two-pass for the 3D general operator, row gather otherwise)."""
-    k = os.environ.get("SA_KERNEL", "")
-    if k == "tile":
-        return "k_numeric_tiles"
-    if k == "chunk":
-        return "k_numeric_chunks"
-    if k == "twopass" or (not k and cfg["d"] == 3 and cfg["ops"] == ("general",)):
-        return "k_element_rows_pipe + k_numeric_rowgather<PRE> (two-pass; time = both)"
+    t = os.environ.get("SA_TUNE", "")
+    if "kernel=rowgather" in t:
+        return "k_numeric_rowgather"
+    if "kernel=twopass" in t or (cfg["d"] == 3 and cfg["ops"] == ("general",)):
+        return ("k_element_rows_pipe + k_numeric_rowgather<PRE> + k_guard_fixup (two-pass; fast general "
+                "operator; time = all three)")
     return "k_numeric_rowgather"
 
 
@@ -197,20 +198,42 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def cpu_baseline(cfg, seconds=12.0):
-    """The oracle port (optv2 semantics, C) on a bounded sample of the same
-    workload: an N_s-refinement of the same mesh family, all host threads."""
+def host_runtime():
+    """What the CPU baseline ran on: cores, numpy/OpenBLAS build and core type
+    (BASELINE.md section 3)."""
+    import io
+    from contextlib import redirect_stdout
+
+    info = {"os_cpu_count": os.cpu_count(), "openblas_coretype": os.environ.get("OPENBLAS_CORETYPE"),
+            "numpy": np.__version__}
+    try:
+        buf = io.StringIO()
+        with redirect_stdout(buf):
+            np.show_runtime()
+        info["numpy_show_runtime"] = buf.getvalue().strip()[:2000]
+    except Exception as exc:  # pragma: no cover
+        info["numpy_show_runtime"] = f"unavailable: {exc}"
+    try:
+        with open("/proc/cpuinfo") as f:
+            info["cpu_model"] = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), None)
+    except OSError:
+        pass
+    return info
+
+
+def host_problem(cfg):
+    """The config's full mesh and coefficients on the host (the same seeded
+    arrays the GPU arm generates on the device: sa_kuhn_mesh is bitwise the
+    host generator, tests/test_gpu_parity.py::test_device_mesh_generator_bitwise)."""
     from oracle import oracle as O
 
     import paper_1401_3301_b200 as P
 
-    d = cfg["d"]
-    n_s = {2: 1000, 3: 60}[d] if cfg["n"] > ({2: 1000, 3: 60}[d]) else cfg["n"]
-    q, me = P.hypercube_arrays(d, n_s)
-    q = P.jitter_interior(q, n_s, 0.2 if d == 2 else 0.15, cfg["seed"])
+    d, n = cfg["d"], cfg["n"]
+    q, me = P.hypercube_arrays(d, n)
+    q = P.jitter_interior(q, n, 0.2 if d == 2 else 0.15, cfg["seed"])
     vols = O.volumes(q, me)
-    nq, nme = q.shape[1], me.shape[1]
-    threads = os.cpu_count() or 1
+    nq = q.shape[1]
     ops = []
     for op in cfg["ops"]:
         if op == "mass":
@@ -220,38 +243,63 @@ def cpu_baseline(cfg, seconds=12.0):
         elif op == "elastic":
             ops.append(O.OracleOp("elastic", d, vols, lamb=np.ones(nq), mu=np.full(nq, 0.5)))
         else:
-            sample = P.Mesh(q, me, vols)
-            k = make_kernels(cfg, sample)[0]
-            A = k.A if k.A is not None else np.broadcast_to(k.A_const, (nq, 3, 3))
-            ops.append(O.OracleOp("general", d, vols, A=A, b=k.b, c=k.c, a0=k.a0))
+            f = general_coeffs(cfg, nq)
+            ops.append(O.OracleOp("general", d, vols, **f))
+    return q, me, ops
+
+
+def cpu_baseline(cfg, runs=1, prob=None):
+    """The oracle port (oracle/p1_oracle.c: optv2 semantics -- element-major
+    triplets, stable per-row sort, left-to-right fold, zero drop) over the
+    config's FULL mesh on all host threads; the median of ``runs`` full
+    assemblies (every operator of the config)."""
+    from oracle import oracle as O
+
+    O.build()
+    q, me, ops = prob if prob is not None else host_problem(cfg)
+    nme = me.shape[1]
+    threads = os.cpu_count() or 1
     times = []
-    t_end = time.perf_counter() + seconds
-    while True:
+    for _ in range(max(1, runs)):
         t0 = time.perf_counter()
         for op in ops:
             O.assemble(q, me, op, nthreads=threads)
         times.append(time.perf_counter() - t0)
-        if time.perf_counter() > t_end and len(times) >= 3:
-            break
     med = statistics.median(times)
     return {"value": nme / med, "unit": "elements/s", "cores": threads, "kind": "port",
-            "sample": f"{d}D N={n_s} jittered Kuhn mesh ({nme} elements), ops {'+'.join(cfg['ops'])}, "
-                      f"median of {len(times)} full optv2 assemblies (C oracle, {threads} threads)"}
+            "sample": f"the full config: {cfg['d']}D N={cfg['n']} jittered Kuhn mesh ({nme} elements), ops "
+                      f"{'+'.join(cfg['ops'])}; median of {len(times)} full optv2 assemblies (C oracle restating the "
+                      f"reference, {threads} threads)", "seconds_per_assembly": med, "host": host_runtime()}
 
 
 def run_reference(args, cfg):
+    """--impl reference: the reference algorithm's CPU implementation (the
+    oracle port; the reference itself is single-threaded numpy)
+    on the SAME full config, each step one full assembly, rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from oracle import oracle as O
 
     O.build()
-    per_step = max(2.0, 60.0 / max(1, args.steps + args.warmup))
-    base = cpu_baseline(cfg, seconds=per_step * (args.steps + args.warmup))
-    line = {"metric": METRIC, "value": base["value"], "unit": "elements/s", "impl": "reference",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "dtype": "f64", "data": "synthetic", "config": {"workload": args.config, **config_desc(cfg)},
-            "cpu_baseline": base, "e2e": {"value": base["value"], "unit": "elements/s",
+    prob = host_problem(cfg)
+    for _ in range(args.warmup):
+        cpu_baseline(cfg, 1, prob)
+    steps = []
+    for _ in range(args.steps):
+        steps.append(cpu_baseline(cfg, 1, prob)["seconds_per_assembly"])
+    nme = prob[1].shape[1]
+    total = sum(steps)
+    value = nme * len(steps) / total
+    base = {"value": value, "unit": "elements/s", "cores": os.cpu_count() or 1, "kind": "port",
+            "sample": f"the full config ({nme} elements) every step: {args.steps} timed full optv2 assemblies after "
+                      f"{args.warmup} untimed (C oracle restating the reference, all host threads)",
+            "host": host_runtime()}
+    line = {"metric": METRIC, "value": value, "unit": "elements/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(steps),
+            "higher_is_better": True, "scaling": args.scaling, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, **config_desc(cfg), "nme": nme, "same_config": True},
+            "cpu_baseline": base, "e2e": {"value": value, "unit": "elements/s",
                                           "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "vs_baseline": None}
     print(json.dumps(line), flush=True)
@@ -268,12 +316,13 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C5", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the numeric phase directly instead of "
                     "replaying its CUDA graph")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N > 1: weak = per-GPU work fixed (refined global mesh), strong = the config mesh split N ways")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="N > 1: strong = the config mesh split N ways (BASELINE C5: 'row-block sharded at "
+                         "1/2/4/8 B200'), weak = per-GPU work fixed (refined global mesh)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -301,6 +350,9 @@ def main():
         if same_gpu:
             dist.init_process_group("gloo")
         else:
+            # NCCL's own log shows the communicator (ranks, transports)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
 
     # Weak scaling (default): the global mesh is refined so each rank's row
@@ -450,7 +502,7 @@ def main():
                    "exact_zero_entries": zeros, "parallelism": f"row-blocks x{world}",
                    "plan": {k: v for k, v in plan.stats().items()
                             if k in ("incidences", "max_row_nodes", "nodes", "nnz") or v},
-                   "kernel": os.environ.get("SA_KERNEL", "default"),
+                   "kernel": os.environ.get("SA_TUNE", "default"),
                    "l2": "flushed between timed steps (256 MiB write); inputs+outputs > L2",
                    "timing": "per-step CUDA events on the launching stream, summed; max over ranks",
                    "launch": "CUDA graph replay of the numeric phase" if graph is not None else "direct"},
@@ -459,7 +511,7 @@ def main():
         "symbolic_cold_ms": t_sym_cold_ms,
         "numeric_ms": ms_per_step,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, **profiled_traffic(args.config), "peak_kind": peak_kind,
+                     "frac": achieved / peak, **profiled_traffic(args.config, numeric_kernels(cfg).split()[0], world), "peak_kind": peak_kind,
                      "algorithmic_bytes": b_num, "kernel": numeric_kernels(cfg),
                      "frac_of_8TBps_nominal": achieved / 8000.0},
         "gpu_launches": launches,

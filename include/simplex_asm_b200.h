@@ -40,7 +40,14 @@ enum {
     SA_OP_MASS = 1,      /* MassKernel       kernels.py:281-303 (mass_kernel :68-78)      */
     SA_OP_STIFF = 2,     /* StiffnessKernel  kernels.py:306-329 (stiffness_kernel :81-88) */
     SA_OP_ELASTIC = 4,   /* ElasticKernel    kernels.py:332-387 (elastic_kernel :155-172) */
-    SA_OP_GENERAL = 8    /* -div(A grad u)+div(b u)+c.grad u+a0 u */
+    SA_OP_GENERAL = 8,   /* -div(A grad u)+div(b u)+c.grad u+a0 u */
+    /* modifier: the general operator's element values in the reference's
+     * operation order (bitwise the oracle).  Without it the general operator's
+     * local matrices use fused multiply-adds: values within a few ulp of the
+     * contributions, the exact-zero pattern still the reference's (guarded
+     * rows are recomputed in reference order).  Mass, stiffness and elastic
+     * are always bitwise. */
+    SA_OP_EXACT = 16
 };
 
 /* OpenBLAS kernel family whose dgesv/dgetrf bits the gradients reproduce
@@ -88,9 +95,9 @@ int sa_plan_info(const sa_plan *plan, int64_t *nrows, int64_t *nnz_structural,
 /* Structural CSR of the block (indptr relative, int64 (nrows+1); indices
  * global column dofs int32 (nnz)), into caller-allocated device buffers. */
 int sa_plan_pattern(const sa_plan *plan, int64_t *indptr_dev, int32_t *indices_dev, void *stream);
-/* Diagnostics: out[0..n) = {tile templates, tile templates verified, every
- * node <= 64 incidences, incidences, tile template words, max row nodes,
- * nodes, nnz, chunk plan ok, chunks, chunk templates, chunk template words}. */
+/* Diagnostics: out[0..n) = {incidences, max row nodes, nodes, nnz, warp
+ * interleaved records, two-pass slots, every element batch staged (0/1),
+ * largest batch vertex count}. */
 int sa_plan_stats(const sa_plan *plan, int64_t *out, int n);
 int sa_plan_destroy(sa_plan *plan);
 
@@ -113,6 +120,11 @@ typedef struct sa_coeffs {
      * [A (3x3 row-major, zero-padded for d < 3) | b (3) | c (3) | a0], one
      * 128-byte line per node; overrides A/b/c/a0 when non-NULL */
     const double *gen_packed;
+    /* elastic, optional: per-element Lame sums already scaled, exactly the
+     * reference ElasticKernel's arrays lambs = (sum_g lamb_g) * vols/(d+1)
+     * and mus (kernels.py:354-356), (nme,) each; override lamb/mu */
+    const double *lambs_e;
+    const double *mus_e;
 } sa_coeffs;
 
 /* Assemble the values of every structural entry of the block into

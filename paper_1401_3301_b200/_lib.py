@@ -19,6 +19,7 @@ from .errors import (
 
 SA_OK, SA_ERR_DEGENERATE, SA_ERR_INDEX_RANGE, SA_ERR_CAPACITY, SA_ERR_ARG, SA_ERR_CUDA, SA_ERR_NOMEM = range(7)
 SA_OP_MASS, SA_OP_STIFF, SA_OP_ELASTIC, SA_OP_GENERAL = 1, 2, 4, 8
+SA_OP_EXACT = 16
 SA_CORE = {"SkylakeX": 0, "Haswell": 1}
 
 # every symbol include/simplex_asm_b200.h declares
@@ -39,6 +40,8 @@ class SaCoeffs(ctypes.Structure):
         ("A", ctypes.c_void_p), ("b", ctypes.c_void_p), ("c", ctypes.c_void_p), ("a0", ctypes.c_void_p),
         ("A_const", ctypes.c_double * 9), ("a0_const", ctypes.c_double),
         ("gen_packed", ctypes.c_void_p),
+        ("lambs_e", ctypes.c_void_p),
+        ("mus_e", ctypes.c_void_p),
     ]
 
 

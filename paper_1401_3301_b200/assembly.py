@@ -55,6 +55,10 @@ def _as_descriptor(mesh, kernel):
         for a in range(kernel.W.shape[0]):
             w[np.asarray(mesh.me[a])] = kernel.W[a]
         return _k.MassKernel(mesh, w)
+    if name == "ElasticKernel" and hasattr(kernel, "lambs") and hasattr(kernel, "mus"):
+        # reference ElasticKernel keeps only the per-element scaled Lame sums
+        # (kernels.py:354-356): pass them through unchanged (bitwise)
+        return _k.ElasticKernel.per_element(mesh, kernel.lambs, kernel.mus)
     if name == "ScalarAsVectorKernel":
         return _as_descriptor(mesh, kernel._kernel)
     raise TypeError(f"assemble_b200 cannot use a {name}; build the kernel with "

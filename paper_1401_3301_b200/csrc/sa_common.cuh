@@ -44,6 +44,12 @@ int set_error(int status, const char *fmt, ...);
                                    cudaGetErrorString(_e));                                 \
     } while (0)
 
+// SA_TUNE="key=value,..." -- the library's single developer/test switch
+// (keys: kernel=rowgather|twopass, symfast=0|1, winc=0|1); unset in
+// production, every default is the measured best
+int tune_int(const char *key, int dflt);
+bool tune_is(const char *key, const char *value);
+
 inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
 
 // Device-wide exclusive scan of int64 (in place allowed): out[i] = sum_{j<i} in[j],

@@ -15,12 +15,10 @@
 #include <climits>
 #include <cstdlib>
 #include <cstring>
-#include <unordered_map>
 #include <vector>
 
 #include "sa_common.cuh"
 #include "sa_geometry.cuh"
-#include "sa_radix.cuh"
 
 using namespace sa;
 
@@ -67,29 +65,6 @@ struct sa_plan {
     IncRec *winc = nullptr;       // warp-interleaved records (padded to each warp's max degree)
     int64_t *wseg = nullptr;      // (nwarps+1) record offset of each warp of 32 node rows
     int64_t n_winc = 0;
-    // block numeric kernel: compact incidences + fold program
-    uint32_t *inc_e = nullptr;    // (n_inc) e | alpha<<30
-    uint16_t *fold = nullptr;     // ((d+1) n_inc) per slot: u | beta<<6 | last<<8
-    bool fold_ok = false;         // every node has <= 64 incidences
-    // fold templates (tile kernel)
-    bool tm_ok = false;
-    int64_t n_templates = 0, tm_nwords = 0;
-    int tile_rows = 0;
-    uint32_t *tile_e0 = nullptr, *tile_tm = nullptr, *tm_off = nullptr, *tm = nullptr;
-    // per tile size R = 2^c (c = 0..5): max incidences / node-level entries in one tile of R rows
-    int64_t tile_max_inc[6] = {0, 0, 0, 0, 0, 0};
-    int64_t tile_max_ent[6] = {0, 0, 0, 0, 0, 0};
-    // chunk kernel
-    bool ck_ok = false;
-    unsigned ck_emin = 0, ck_emax = 0;
-    int ck_C = 0;
-    int64_t ck_nchunks = 0, ck_ntemplates = 0, ck_nwords = 0;
-    uint32_t *ck_tm = nullptr, *ck_pb = nullptr, *ck_tm_off = nullptr, *ck_tmw = nullptr;
-    unsigned *ck_flags = nullptr;  // nrec record flags + 1 ticket
-    uint32_t *ck_rs = nullptr;     // first record index per chunk
-    int64_t ck_nrec = 0;
-    int64_t ck_maxw = 0;           // largest chunk template (words)
-    unsigned ck_epoch = 0;         // bumped per launch
     // two-pass numeric ("element rows"): incidence slot of every (element, alpha)
     // of the block's element range, and the per-incidence local-row buffer
     uint4 *epos = nullptr;         // (e_hi - e_lo): slot t of (e, alpha) in inc, or ~0u
@@ -105,11 +80,10 @@ struct sa_plan {
     uint32_t *eb_loc = nullptr;
     int eb_maxn = 0;
     bool eb_allfit = false;        // every batch staged (no direct-gather fallback compiled in)
-    // overlap of the element pass (compute) with the fold (DRAM): element
-    // batch chunks and the warp-aligned row segments whose elements they hold
-    std::vector<int64_t> ov_bcut, ov_wcut;   // (K+1) batch cuts, (K+1) warp cuts
-    cudaStream_t ov_stream = nullptr;
-    std::vector<cudaEvent_t> ov_events;
+    // fast general operator: rows whose zero guard tripped (recomputed in
+    // reference order by k_guard_fixup)
+    uint32_t *gd_flag_rows = nullptr;
+    int *gd_nflag = nullptr;
 };
 
 // numeric-phase arguments (shared by the per-dimension translation units)
@@ -126,7 +100,6 @@ struct NumArgs {
     const int64_t *colptr;
     const int64_t *indptr;
     const int32_t *cols;  // node-level sorted neighbour nodes (row-gather coordinate cache)
-    int dbg;              // diagnostics (SA_DBG): 1 = loads only, 2 = loads + element math, no folds, 3 = stores only
     int acc_stride;  // smem accumulator rows per output (m*m*max_deg)
     double *vals[2];
     int64_t *counters;
@@ -137,6 +110,7 @@ struct NumArgs {
     const double *A; const double *b; const double *c; const double *a0;
     double A_const[9]; double a0_const;
     const double *gen_packed;  // (nq, 16) AoS [A(9) b(3) c(3) a0] or NULL
+    const double *lambs_e, *mus_e;   // elastic: per-element scaled Lame sums (reference ElasticKernel) or NULL
     // two-pass numeric: element pass writes local rows to kbuf (stride kstride
     // doubles per incidence), the ordered fold pass reads them
     double *kbuf; int kstride;
@@ -147,14 +121,19 @@ struct NumArgs {
     int eb_maxn;
     int eb_allfit;
     int64_t eb_b0, eb_b1;      // element-pass batch range of this launch
-    int64_t row0, row1;        // fold (PRE) row range of this launch (row0 % 32 == 0)
     double mass_coef_diag, mass_coef_off;  // 2/((d+1)(d+2)(d+3)), 1/(...) as Python computes them
     double mass_wc;  // constant weight: (wsum + w) + w, the same for every (alpha, beta)
+    int exact;       // general operator: reference-order (bitwise) element values
+    int *nflag;          // fast general operator: guarded-row count + list
+    uint32_t *flag_rows;
 };
 
 namespace {
 
 constexpr int MAXC = 255;  // 8-bit ranks: at most 255 distinct neighbour nodes per node
+// fast general operator: |entry| <= SA_GUARD_TAU * (sum of |contributions| of
+// its row) sends the row to the reference-order recomputation
+constexpr double SA_GUARD_TAU = 1e-9;
 
 inline int set_device(int dev)
 {
@@ -439,180 +418,6 @@ __global__ void k_winc_fill(const typename IdxT<D>::type *__restrict__ me, const
     }
 }
 
-// Fold program of node row nl: for each column k (ascending), the
-// contributing (incidence u, local vertex beta) pairs in ascending element
-// order, as u | beta << 6; the last pair of each column has bit 8 set.
-template <int D>
-__global__ void k_fold_lists(const int64_t *__restrict__ inc_ptr, const uint2 *__restrict__ inc, int64_t nnodes,
-                             const int64_t *__restrict__ colptr, uint32_t *__restrict__ inc_e,
-                             uint16_t *__restrict__ fold, unsigned long long *too_many)
-{
-    int64_t nl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (nl >= nnodes) return;
-    const int64_t t0 = inc_ptr[nl];
-    const int ni = (int)(inc_ptr[nl + 1] - t0);
-    for (int u = 0; u < ni; ++u) inc_e[t0 + u] = inc[t0 + u].x;
-    if (ni > 64) { atomicOr(too_many, 1ull); return; }
-    const int deg = (int)(colptr[nl + 1] - colptr[nl]);
-    uint16_t *out = fold + (int64_t)(D + 1) * t0;
-    int w = 0;
-    for (int k = 0; k < deg; ++k) {
-        int last = -1;
-        for (int u = 0; u < ni; ++u) {
-            const unsigned r = inc[t0 + u].y;
-            for (int b = 0; b <= D; ++b)
-                if ((int)((r >> (8 * b)) & 0xff) == k) { out[w] = (uint16_t)(u | (b << 6)); last = w; ++w; }
-        }
-        if (last >= 0) out[last] |= 256;
-    }
-}
-
-// ---- tile templates -------------------------------------------------------
-// A tile is R consecutive node rows, processed by one warp.  Its template
-// (relative to the tile's smallest element id e_base) holds
-//   w[0] = n_elem | nrows << 8 | nslots << 16,  w[1] = NE node-level entries
-//   w[2 .. 2+ne)            de[j]: the tile's distinct elements, ascending
-//   w[2+ne .. 2+2ne)        per element: 4 x 8-bit slot id of local row
-//                           alpha = 0..3 (0xff: vertex not in the tile)
-//   w[2+2ne .. 2+2ne+2NI)   per slot (= incidence, row-major, ascending
-//                           element per row): 4 x 16-bit fold positions,
-//                           one per local column beta
-//   w[PB .. PB+nrows)       per row: deg | entb << 16
-//   w[OB .. OB+(NE+2)/2)    NE+1 uint16 entry offsets into the fold array
-//   w[LB .. LB+17)          33 uint16: lane l sums entries [ls[l], ls[l+1]),
-//                           split so every lane gets ~1/32 of the contributions
-// The fold array of a tile is entry-major: entry k's contributions occupy
-// [off[k], off[k+1]) in ascending element order.  Element lanes scatter their
-// local rows straight into it; row lanes then sum contiguous runs.
-// Tiles with equal templates share one copy: all interior tiles of a
-// structured mesh collapse to a few dozen.
-__device__ __forceinline__ uint64_t fnv_step(uint64_t h, uint32_t x)
-{
-#pragma unroll
-    for (int i = 0; i < 4; ++i) { h ^= (x >> (8 * i)) & 0xff; h *= 1099511628211ull; }
-    return h;
-}
-
-constexpr int TILE_MAX_ELEM = 255;
-
-__host__ __device__ inline int64_t tile_stride_bound(int64_t NI, int64_t NE, int64_t R)
-{
-    return 2 + 2 * (NI < TILE_MAX_ELEM ? NI : TILE_MAX_ELEM) + 2 * NI + R + (NE + 2) / 2 + 17 + 4;
-}
-
-template <int D>
-__global__ void k_tile_build(const int64_t *__restrict__ inc_ptr, const uint32_t *__restrict__ inc_e,
-                             const uint16_t *__restrict__ fold, const int64_t *__restrict__ colptr, int64_t nnodes,
-                             int R, int64_t ntiles, int stride, uint32_t *__restrict__ scratch,
-                             uint32_t *__restrict__ words_out, uint64_t *__restrict__ sig,
-                             uint32_t *__restrict__ tile_e0, unsigned long long *fail)
-{
-    const int64_t T = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (T >= ntiles) return;
-    const int64_t r0 = T * R;
-    const int nr = (int)min((int64_t)R, nnodes - r0);
-    uint32_t *w = scratch + T * (int64_t)stride;
-    const int64_t t0 = inc_ptr[r0];
-    const int NI = (int)(inc_ptr[r0 + nr] - t0);
-    const int64_t c0 = colptr[r0];
-    const int NE = (int)(colptr[r0 + nr] - c0);
-    uint32_t el[TILE_MAX_ELEM];
-    int ne = 0;
-    bool bad = NI > 254 || (D + 1) * NI > 65535 || NE > 65534;
-    for (int i = 0; i < NI && !bad; ++i) {
-        const uint32_t e = inc_e[t0 + i] & 0x3fffffffu;
-        int lo = 0, hi = ne;
-        while (lo < hi) { int mid = (lo + hi) >> 1; if (el[mid] < e) lo = mid + 1; else hi = mid; }
-        if (lo < ne && el[lo] == e) continue;
-        if (ne == TILE_MAX_ELEM) { bad = true; break; }
-        for (int k = ne; k > lo; --k) el[k] = el[k - 1];
-        el[lo] = e;
-        ++ne;
-    }
-    if (bad) { atomicOr(fail, 1ull); words_out[T] = 0; return; }
-    const uint32_t eb = ne ? el[0] : 0u;
-    tile_e0[T] = eb;
-    w[0] = (uint32_t)ne | ((uint32_t)nr << 8) | ((uint32_t)NI << 16);
-    w[1] = (uint32_t)NE;
-    for (int j = 0; j < ne; ++j) { w[2 + j] = el[j] - eb; w[2 + ne + j] = 0xffffffffu; }
-    for (int i = 0; i < NI; ++i) {
-        const uint32_t r = inc_e[t0 + i];
-        const uint32_t e = r & 0x3fffffffu, alpha = r >> 30;
-        int lo = 0, hi = ne;
-        while (lo < hi) { int mid = (lo + hi) >> 1; if (el[mid] < e) lo = mid + 1; else hi = mid; }
-        uint32_t &sw = w[2 + ne + lo];
-        sw = (sw & ~(0xffu << (8 * alpha))) | ((uint32_t)i << (8 * alpha));
-    }
-    const uint32_t SB = 2 + 2 * ne, PB = SB + 2 * NI, OB = PB + nr, LB = OB + ((NE + 2) >> 1);
-    const uint32_t end = LB + 17;
-    for (uint32_t x = SB; x < end; ++x) w[x] = 0;
-    for (int row = 0; row < nr; ++row) {
-        const int64_t ip = inc_ptr[r0 + row];
-        const int ni = (int)(inc_ptr[r0 + row + 1] - ip);
-        const int deg = (int)(colptr[r0 + row + 1] - colptr[r0 + row]);
-        const int incb = (int)(ip - t0);
-        const int entb = (int)(colptr[r0 + row] - c0);
-        w[PB + row] = (uint32_t)deg | ((uint32_t)entb << 16);
-        int k = 0;
-        for (int s = 0; s < (D + 1) * ni; ++s) {
-            const uint16_t f = fold[(D + 1) * ip + s];
-            const uint32_t slot = incb + (f & 63), beta = (f >> 6) & 3;
-            const uint32_t pos = (uint32_t)((D + 1) * incb + s);
-            w[SB + 2 * slot + (beta >> 1)] |= pos << (16 * (beta & 1));
-            if (f & 256) {
-                ++k;
-                const uint32_t kg = entb + k;
-                w[OB + (kg >> 1)] |= (pos + 1) << (16 * (kg & 1));
-            }
-        }
-    }
-    // lane starts: lane l takes the entries whose runs start in [l*NC/32, (l+1)*NC/32)
-    {
-        const uint32_t NC = (uint32_t)((D + 1) * NI);
-        int k = 0;
-        for (int l = 0; l <= 32; ++l) {
-            const uint32_t target = (uint32_t)(((uint64_t)NC * l) / 32);
-            while (k < NE && ((w[OB + (k >> 1)] >> (16 * (k & 1))) & 0xffff) < target) ++k;
-            const uint32_t v = l == 32 ? (uint32_t)NE : (uint32_t)k;
-            w[LB + (l >> 1)] |= v << (16 * (l & 1));
-        }
-    }
-    words_out[T] = end;
-    uint64_t h = 1469598103934665603ull;
-    for (uint32_t x = 0; x < end; ++x) h = fnv_step(h, w[x]);
-    sig[T] = h;
-}
-
-__global__ void k_tile_pack(const int64_t *__restrict__ rep, int64_t ntm, const uint32_t *__restrict__ scratch,
-                            int stride, const uint32_t *__restrict__ words, const uint32_t *__restrict__ tm_off,
-                            uint32_t *__restrict__ tm)
-{
-    // one warp per template
-    const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (t >= ntm) return;
-    const uint32_t *src = scratch + rep[t] * (int64_t)stride;
-    uint32_t *dst = tm + tm_off[t];
-    const uint32_t n = words[rep[t]];
-    for (uint32_t i = lane; i < n; i += 32) dst[i] = src[i];
-}
-
-__global__ void k_tile_verify(const uint32_t *__restrict__ scratch, int stride, const uint32_t *__restrict__ words,
-                              int64_t ntiles, const uint32_t *__restrict__ tile_tm,
-                              const uint32_t *__restrict__ tm_off, const uint32_t *__restrict__ tm,
-                              unsigned long long *bad)
-{
-    const int64_t T = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (T >= ntiles) return;
-    const uint32_t *a = scratch + T * (int64_t)stride;
-    const uint32_t *b = tm + tm_off[tile_tm[T]];
-    const uint32_t n = words[T];
-    bool ok = true;
-    for (uint32_t i = lane; i < n; i += 32) ok &= (a[i] == b[i]);
-    if (!__all_sync(0xffffffffu, ok) && lane == 0) atomicOr(bad, 1ull);
-}
-
 // max_i (p[i+1] - p[i]) over a prefix array
 __global__ void k_max_diff(const int64_t *__restrict__ p, int64_t n, unsigned long long *out)
 {
@@ -679,17 +484,33 @@ struct ElemRaw {
     double vol;
     double x[D + 1][D];
     double W[D + 1], lam[D + 1], mu[D + 1];
+    double elam, emu;   // elastic, per-element input (lambs_e/mus_e), used when pre_lm
+    int pre_lm;
     // general: coefficient sums accumulated while loading (in vertex order,
     // as the reference-order restatement sums them) + the per-vertex terms
     double As[D][D], bs[D], cs[D], a0s;
     double bv[D + 1][D], cv[D + 1][D], a0v[D + 1];
 };
 
+// elastic with the reference's per-element lambs/mus (kernels.py:354-356)
+template <int D, int OPS>
+__device__ __forceinline__ void element_load_lm(const NumArgs &a, int64_t e, ElemRaw<D> &r)
+{
+    if constexpr ((OPS & OP_ELASTIC) != 0) {
+        r.pre_lm = a.lambs_e != nullptr;
+        if (r.pre_lm) {
+            r.elam = __ldg(a.lambs_e + e);
+            r.emu = __ldg(a.mus_e + e);
+        }
+    }
+}
+
 template <int D, int OPS>
 __device__ __forceinline__ void element_load1(const NumArgs &a, int64_t e, ElemRaw<D> &r)
 {
     load_element<D>((const typename IdxT<D>::type *)a.me, e, r.v);
     r.vol = __ldg(a.vols + e);
+    element_load_lm<D, OPS>(a, e, r);
 }
 
 // nodal coefficients of the element's vertices (r.v loaded)
@@ -770,13 +591,18 @@ __device__ __forceinline__ bool element_compute(const ElemRaw<D> &r, ElemGeo<D> 
         for (int k = 1; k <= D; ++k) g.wsum = SA_ADD(g.wsum, r.W[k]);
     }
     if constexpr ((OPS & OP_ELASTIC) != 0) {
-        // lambs = (sum_k lamb_k) * (vols / (d+1))   kernels.py:354-356
-        const double scale = __ddiv_rn(r.vol, (double)(D + 1));
-        double ls = r.lam[0], ms = r.mu[0];
+        if (r.pre_lm) {
+            g.lambs = r.elam;
+            g.mus = r.emu;
+        } else {
+            // lambs = (sum_k lamb_k) * (vols / (d+1))   kernels.py:354-356
+            const double scale = __ddiv_rn(r.vol, (double)(D + 1));
+            double ls = r.lam[0], ms = r.mu[0];
 #pragma unroll
-        for (int k = 1; k <= D; ++k) { ls = SA_ADD(ls, r.lam[k]); ms = SA_ADD(ms, r.mu[k]); }
-        g.lambs = SA_MUL(ls, scale);
-        g.mus = SA_MUL(ms, scale);
+            for (int k = 1; k <= D; ++k) { ls = SA_ADD(ls, r.lam[k]); ms = SA_ADD(ms, r.mu[k]); }
+            g.lambs = SA_MUL(ls, scale);
+            g.mus = SA_MUL(ms, scale);
+        }
     }
     if constexpr ((OPS & OP_GENERAL) != 0) {
 #pragma unroll
@@ -968,21 +794,17 @@ __device__ __forceinline__ void krow_runtime(const NumArgs &a, const ElemGeo<D> 
 // accumulators indexed by the 8-bit column ranks stored with each incidence.
 // Used when a node has more than 31 incidences or the block kernel's shared
 // memory does not fit.
-template <int D, int M, int OPS, int CORE, int ILP, int MINB, bool PRE = false, bool LEAN = false>
+template <int D, int M, int OPS, int CORE, int ILP, int MINB, bool PRE = false, bool LEAN = false, bool GUARD = false>
 __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
 {
-    // LEAN: no diagnostics and a constant mass weight, known at compile time
-    // (the local copy is scalar-replaced; w == nullptr and dbg == 0 fold the
-    // weight loads and the diagnostic branches away)
+    // LEAN: a constant mass weight, known at compile time (the local copy is
+    // scalar-replaced; w == nullptr folds the weight loads away)
     NumArgs a = a_in;
-    if constexpr (LEAN) {
-        a.w = nullptr;
-        a.dbg = 0;
-    }
+    if constexpr (LEAN) a.w = nullptr;
     constexpr int NOUT = n_outputs<OPS>();
     extern __shared__ double smem_acc[];
     const int tid = threadIdx.x, lane = tid & 31;
-    const int64_t nl = (PRE ? a.row0 : 0) + blockIdx.x * (int64_t)blockDim.x + tid;
+    const int64_t nl = blockIdx.x * (int64_t)blockDim.x + tid;
     // Accumulators: per warp and output a plane of 32 lane rows of S doubles;
     // lane j's dof row l, column k at wacc[o*32*S + j*S + l*M*deg + k].  When
     // the warp's rows all have degree d0, S = M*M*d0 and the plane IS the
@@ -991,7 +813,7 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
     // row (odd, so lane strides hit distinct banks) and rows store their own
     // segments.
     const unsigned full = 0xffffffffu;
-    const bool active = nl < (PRE ? a.row1 : a.nnodes);
+    const bool active = nl < a.nnodes;
     const int64_t c0 = active ? a.colptr[nl] : 0;
     const int deg = active ? (int)(a.colptr[nl + 1] - c0) : -1;
     // the row's CSR base, loaded with the degree (independent loads: one
@@ -1008,18 +830,22 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
     int nz[NOUT];
 #pragma unroll
     for (int o = 0; o < NOUT; ++o) nz[o] = 0;
+    double rbound = 0.0;   // GUARD: sum over the row's contributions of |K[alpha][beta]|
     if (active) {
         const int deg_stride = M * deg;
         for (int o = 0; o < NOUT; ++o)
             for (int k = 0; k < M * deg_stride; ++k) wacc[o * 32 * S + k] = 0.0;
-        const int64_t t1 = a.dbg >= 3 ? inc0 : inc1;   // 3: stores only, 4: neither
+        const int64_t t1 = inc1;
         int64_t emin = INT64_MAX;
         constexpr int MM = M * M;
-        double dsum = 0.0;
         constexpr int VPR = (D + 1) * NOUT * MM;
         // fold one local row set into the row accumulators (ranks: 8-bit
         // column rank of each element vertex within this row)
         auto accum = [&](const double(&vals)[VPR], unsigned ranks) {
+            if constexpr (GUARD) {   // fast values: the zero guard's magnitude, sum of |contributions|
+#pragma unroll
+                for (int i = 0; i < VPR; ++i) rbound += fabs(vals[i]);
+            }
 #pragma unroll
             for (int b = 0; b <= D; ++b) {
                 const int r = (ranks >> (8 * b)) & 0xff;
@@ -1033,14 +859,6 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
             }
         };
         auto fold = [&](const ElemRaw<D> &x, uint2 rec) {
-            if (a.dbg == 1) {   // diagnostics: memory traffic only
-#pragma unroll
-                for (int b = 0; b <= D; ++b)
-#pragma unroll
-                    for (int c = 0; c < D; ++c) dsum += x.x[b][c];
-                dsum += x.vol + (double)x.v[0] + (double)rec.y;
-                return;
-            }
             ElemGeo<D> g;
             const int64_t e = rec.x & 0x3fffffffu;
             if (element_compute<D, OPS, CORE>(x, g)) emin = min(emin, e);
@@ -1049,11 +867,6 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
                 element_krow_sel<D, OPS>(a, g, rec.x >> 30, vals);
             else
                 krow_runtime<D, M, OPS>(a, g, rec.x >> 30, vals);
-            if (a.dbg == 2) {   // diagnostics: no folds
-#pragma unroll
-                for (int i = 0; i < (D + 1) * NOUT * MM; ++i) dsum += vals[i];
-                return;
-            }
             accum(vals, rec.y);
         };
         const int64_t t0 = inc0;
@@ -1073,6 +886,7 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
                 if constexpr (D >= 2) x.v[2] = (int)(unsigned)u2;
                 if constexpr (D >= 3) x.v[3] = (int)(unsigned)(u2 >> 32);
                 x.vol = __longlong_as_double((long long)u3);
+                element_load_lm<D, OPS>(a, rec.x & 0x3fffffffu, x);
             } else {
                 rec = __ldg(a.inc + t);
                 element_load1<D, OPS>(a, rec.x & 0x3fffffffu, x);
@@ -1090,7 +904,7 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
                 const double *src = a.kbuf + slot * a.kstride;
                 if constexpr (VPR % 4 == 0) {
 #pragma unroll
-                    for (int i = 0; i < VPR; i += 4) ldg256(src + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+                    for (int i = 0; i < VPR; i += 4) ldg256_cs(src + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
                 } else if constexpr (VPR % 2 == 0) {
 #pragma unroll
                     for (int i = 0; i < VPR; i += 2) {
@@ -1110,7 +924,7 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int64_t slot = sb + 32 * (t + u - t0);
-                    rk[u] = __ldg(a.tp_rank + slot);
+                    rk[u] = __ldcs(a.tp_rank + slot);
                     loadk(slot, v[u]);
                 }
 #pragma unroll
@@ -1119,7 +933,7 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
             for (; t < t1; ++t) {
                 double v[VPR];
                 const int64_t slot = sb + 32 * (t - t0);
-                const unsigned rk = __ldg(a.tp_rank + slot);
+                const unsigned rk = __ldcs(a.tp_rank + slot);
                 loadk(slot, v);
                 accum(v, rk);
             }
@@ -1165,12 +979,21 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
             fold(x1, r1);
         }
         if (emin != INT64_MAX) atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)emin);
-        if (a.dbg) wacc[0] = dsum;
     }
     // Stores (see the accumulator layout above)
     __syncwarp();
-    if (a.dbg == 4) {   // diagnostics: metadata + zero-init only, no stores
-    } else if (uniform) {
+    if constexpr (GUARD) {
+        // an entry this small relative to its row's contributions may be an
+        // exact zero of the reference-order sum: the row is recomputed in
+        // reference order (k_guard_fixup) and its zeros counted there
+        if (active) {
+            bool flag = false;
+            const double thr = SA_GUARD_TAU * rbound;
+            for (int k = 0; k < M * M * deg; ++k) flag |= fabs(wacc[k]) <= thr;
+            if (flag) a.flag_rows[atomicAdd(a.nflag, 1)] = (uint32_t)nl;
+        }
+    }
+    if (uniform) {
         const int64_t base = __shfl_sync(full, row_base, 0);
         const double *plane = wacc - lane * S;
         for (int i = lane; i < 32 * S; i += 32) {
@@ -1178,7 +1001,7 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
             for (int o = 0; o < NOUT; ++o) {
                 const double val = plane[o * 32 * S + i];
                 a.vals[o][base + i] = val;
-                nz[o] += (val == 0.0);
+                if constexpr (!GUARD) nz[o] += (val == 0.0);
             }
         }
     } else if (active) {
@@ -1189,7 +1012,7 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
                 for (int k = 0; k < M * deg; ++k) {
                     const double val = wacc[o * 32 * S + l * M * deg + k];
                     out[p + k] = val;
-                    nz[o] += (val == 0.0);
+                    if constexpr (!GUARD) nz[o] += (val == 0.0);
                 }
             }
         }
@@ -1218,13 +1041,19 @@ __device__ __forceinline__ void st256(double *p, double a, double b, double c, d
 {
     asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
+// streaming variants (evict-first): data touched once -- the two-pass local
+// rows, slot maps -- should not push the staged vertex records out of L2
+__device__ __forceinline__ void st256_cs(double *p, double a, double b, double c, double d)
+{
+    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
 
 template <int VPR>
 __device__ __forceinline__ void store_row(double *dst, const double (&vals)[VPR])
 {
     if constexpr (VPR % 4 == 0) {
 #pragma unroll
-        for (int i = 0; i < VPR; i += 4) st256(dst + i, vals[i], vals[i + 1], vals[i + 2], vals[i + 3]);
+        for (int i = 0; i < VPR; i += 4) st256_cs(dst + i, vals[i], vals[i + 1], vals[i + 2], vals[i + 3]);
     } else if constexpr (VPR % 2 == 0) {
 #pragma unroll
         for (int i = 0; i < VPR; i += 2) *(double2 *)(dst + i) = make_double2(vals[i], vals[i + 1]);
@@ -1409,52 +1238,90 @@ __device__ __forceinline__ void element_from_stage(const double *__restrict__ vr
     }
 }
 
-template <int D, int M, int OPS, int CORE, int MINB, bool ALLFIT = false>
-__global__ void __launch_bounds__(EB_SIZE, MINB) k_element_rows_batched(NumArgs a)
+
+// General operator, fast mode, from the staged vertex records (EB_REC
+// doubles: q padded to 4 | [A 3x3 | b | c | a0]): gradients bitwise
+// (element_gradients -- the same degeneracy test as exact mode), the local
+// matrix regrouped for fused multiply-adds:
+//   Q_b = s1 As G_b - s2 (bs + b_b),  R_a = s2 (cs + c_a),
+//   K[a][b] = G_a . Q_b + G_b . R_a + (a == b ? cd : co) ((a0s + a0_a) + a0_b)
+// ~210 fp64 instructions for the 16 entries instead of ~370 in reference
+// order.  Rows go to their incidence slots (pos) as in element_rows_store.
+template <int D, int CORE>
+__device__ __forceinline__ bool stage_general_fast(const NumArgs &a, const double *__restrict__ vrec, unsigned lc,
+                                                   double vol, const unsigned (&pos)[4])
 {
-    extern __shared__ double vrec[];
-    const int t = threadIdx.x;
-    const int64_t b = blockIdx.x, i = b * EB_SIZE + t;
-    const bool in = i < a.ne;
-    const int64_t e = a.e_lo + i;
-    // ALLFIT: every batch is staged (the direct-gather fallback is not compiled)
-    const int n = ALLFIT ? max(__ldg(a.eb_count + b), 0) : __ldg(a.eb_count + b);
-    uint4 p = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
-    unsigned lc = 0;
-    ElemRaw<D> x;
-    if (in) {
-        p = __ldg(a.epos + i);
-        x.vol = __ldg(a.vols + e);
-        if (n >= 0) lc = __ldg(a.eb_loc + i);
-        else load_element<D>((const typename IdxT<D>::type *)a.me, e, x.v);
-    }
-    if (n >= 0) {   // uniform per block
-        // the batch's vertex list first (one coalesced load), then every
-        // cp.async of the stage issues without a dependent load
-        __shared__ int sv[EB_CAP + 1];
-        const int32_t *vl = a.eb_verts + b * EB_CAP;
-        for (int s = t; s < n; s += EB_SIZE) sv[s] = __ldg(vl + s);
-        __syncthreads();
-        for (int c = t; c < n * 10; c += EB_SIZE) {
-            const int s = c / 10, h = c - 10 * s;
-            const int64_t vv = sv[s];
-            const double *src = h < 2 ? (const double *)a.qv + vv * 4 + 2 * h : a.gen_packed + vv * 16 + 2 * (h - 2);
-            cp_async16(vrec + s * EB_REC + 2 * h, src);
-        }
-        cp_async_wait_all();
-        __syncthreads();
-    }
-    if (!in) return;
-    const unsigned pos[4] = {p.x, p.y, p.z, p.w};
-    bool any = false;
+    const double *rk[D + 1];
 #pragma unroll
-    for (int k = 0; k <= D; ++k) any |= pos[k] != 0xffffffffu;
-    if (!any) return;
-    if (n >= 0) element_from_stage<D, OPS>(vrec, lc, x);
-    else element_load2<D, OPS>(a, x);
-    ElemGeo<D> g;
-    if (element_compute<D, OPS, CORE>(x, g)) atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)e);
-    element_rows_store<D, M, OPS>(a, g, pos);
+    for (int k = 0; k <= D; ++k) rk[k] = vrec + ((lc >> (8 * k)) & 0xff) * EB_REC;
+    double G[D + 1][D];
+    bool deg;
+    {
+        double x[D + 1][D];
+#pragma unroll
+        for (int k = 0; k <= D; ++k)
+#pragma unroll
+            for (int c = 0; c < D; ++c) x[k][c] = rk[k][c];
+        deg = element_gradients<D, CORE>(x, G);
+    }
+    const double s1 = vol * (1.0 / (D + 1));
+    const double s2 = vol * (1.0 / ((D + 1) * (D + 2)));
+    const double cd = a.mass_coef_diag * vol, co = a.mass_coef_off * vol;
+    double As[D][D], bs[D], cs[D], a0s;
+#pragma unroll
+    for (int k = 0; k <= D; ++k) {
+        const double *w = rk[k] + 4;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+#pragma unroll
+            for (int j = 0; j < D; ++j) As[i][j] = k == 0 ? w[i * 3 + j] : As[i][j] + w[i * 3 + j];
+            bs[i] = k == 0 ? w[9 + i] : bs[i] + w[9 + i];
+            cs[i] = k == 0 ? w[12 + i] : cs[i] + w[12 + i];
+        }
+        a0s = k == 0 ? w[15] : a0s + w[15];
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) As[i][j] *= s1;
+        bs[i] *= -s2;
+        cs[i] *= s2;
+    }
+    double Rv[D + 1][D], ea[D + 1], a0v[D + 1];
+#pragma unroll
+    for (int k = 0; k <= D; ++k) {
+        const double *w = rk[k] + 4;
+#pragma unroll
+        for (int i = 0; i < D; ++i) Rv[k][i] = __fma_rn(s2, w[12 + i], cs[i]);
+        a0v[k] = w[15];
+        ea[k] = a0s + w[15];
+    }
+    double K[D + 1][D + 1];
+#pragma unroll
+    for (int b = 0; b <= D; ++b) {
+        const double *w = rk[b] + 4;
+        double Q[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            double t = __fma_rn(-s2, w[9 + i], bs[i]);
+#pragma unroll
+            for (int j = 0; j < D; ++j) t = __fma_rn(As[i][j], G[b][j], t);
+            Q[i] = t;
+        }
+#pragma unroll
+        for (int al = 0; al <= D; ++al) {
+            double t = (al == b ? cd : co) * (ea[al] + a0v[b]);
+#pragma unroll
+            for (int i = 0; i < D; ++i) t = __fma_rn(G[al][i], Q[i], t);
+#pragma unroll
+            for (int i = 0; i < D; ++i) t = __fma_rn(G[b][i], Rv[al][i], t);
+            K[al][b] = t;
+        }
+    }
+#pragma unroll
+    for (int al = 0; al <= D; ++al)
+        if (pos[al] != 0xffffffffu) store_row<D + 1>(a.kbuf + (int64_t)pos[al] * a.kstride, K[al]);
+    return deg;
 }
 
 // Pipelined batched element pass (every batch staged): persistent blocks
@@ -1471,7 +1338,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int D, int M, int OPS, int CORE, int MINB>
+template <int D, int M, int OPS, int CORE, int MINB, bool FAST = false>
 __global__ void __launch_bounds__(EB_SIZE, MINB) k_element_rows_pipe(NumArgs a)
 {
     extern __shared__ double dyn[];
@@ -1518,9 +1385,9 @@ __global__ void __launch_bounds__(EB_SIZE, MINB) k_element_rows_pipe(NumArgs a)
         lc = 0;
         vol = 0.0;
         if (bb < nb && i < a.ne) {
-            p = __ldg(a.epos + i);
-            lc = __ldg(a.eb_loc + i);
-            vol = __ldg(a.vols + a.e_lo + i);
+            p = __ldcs(a.epos + i);
+            lc = __ldcs(a.eb_loc + i);
+            vol = __ldcs(a.vols + a.e_lo + i);
         }
     };
     uint4 p;
@@ -1546,13 +1413,18 @@ __global__ void __launch_bounds__(EB_SIZE, MINB) k_element_rows_pipe(NumArgs a)
 #pragma unroll
         for (int kk = 0; kk <= D; ++kk) any |= pos[kk] != 0xffffffffu;
         if (i < a.ne && any) {
-            ElemRaw<D> x;
-            x.vol = vol;
-            element_from_stage<D, OPS>(recs + (size_t)(k & 1) * RS, lc, x);
-            ElemGeo<D> g;
-            if (element_compute<D, OPS, CORE>(x, g))
-                atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)(a.e_lo + i));
-            element_rows_store<D, M, OPS>(a, g, pos);
+            if constexpr (FAST && OPS == OP_GENERAL) {
+                if (stage_general_fast<D, CORE>(a, recs + (size_t)(k & 1) * RS, lc, vol, pos))
+                    atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)(a.e_lo + i));
+            } else {
+                ElemRaw<D> x;
+                x.vol = vol;
+                element_from_stage<D, OPS>(recs + (size_t)(k & 1) * RS, lc, x);
+                ElemGeo<D> g;
+                if (element_compute<D, OPS, CORE>(x, g))
+                    atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)(a.e_lo + i));
+                element_rows_store<D, M, OPS>(a, g, pos);
+            }
         }
         p = pn;
         lc = lcn;
@@ -1560,20 +1432,6 @@ __global__ void __launch_bounds__(EB_SIZE, MINB) k_element_rows_pipe(NumArgs a)
         __syncthreads();   // stage k & 1 is rewritten by the records of batch k+2
     }
     cp_async_wait<0>();
-}
-
-// largest element of each warp's 32 rows (incidences are sorted per row)
-__global__ void k_warp_emax(const int64_t *__restrict__ inc_ptr, const uint2 *__restrict__ inc, int64_t nnodes,
-                            unsigned *__restrict__ out)
-{
-    const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t r0 = w * 32;
-    if (r0 >= nnodes) return;
-    const int64_t r1 = min(r0 + 32, nnodes);
-    unsigned m = 0;
-    for (int64_t r = r0; r < r1; ++r)
-        if (inc_ptr[r + 1] > inc_ptr[r]) m = max(m, inc[inc_ptr[r + 1] - 1].x & 0x3fffffffu);
-    out[w] = m;
 }
 
 // element range of the block's incidences: out[0] = min e, out[1] = max e
@@ -1613,219 +1471,6 @@ __global__ void k_tp_slots(const int64_t *__restrict__ inc_ptr, const uint2 *__r
         rank[slot] = rec.y;
     }
 }
-
-// element lane: local row A of the element -> scatter into the fold array
-template <int D, int M, int OPS, int A = 0>
-__device__ __forceinline__ void element_rows_scatter(const NumArgs &a, const ElemGeo<D> &g, unsigned sw,
-                                                     const uint32_t *__restrict__ tm, unsigned sb, double *F, int FS)
-{
-    constexpr int NOUT = n_outputs<OPS>();
-    constexpr int MM = M * M;
-    const unsigned slot = (sw >> (8 * A)) & 0xff;
-    if (slot != 0xff) {
-        double vals[(D + 1) * NOUT * MM];
-        element_krow<D, M, OPS, A>(a, g, vals);
-        const unsigned p01 = __ldg(tm + sb + 2 * slot), p23 = __ldg(tm + sb + 2 * slot + 1);
-#pragma unroll
-        for (int b = 0; b <= D; ++b) {
-            const unsigned pos = ((b < 2 ? p01 : p23) >> (16 * (b & 1))) & 0xffff;
-#pragma unroll
-            for (int o = 0; o < NOUT; ++o)
-#pragma unroll
-                for (int i = 0; i < MM; ++i) F[(o * FS + pos) * MM + i] = vals[(b * NOUT + o) * MM + i];
-        }
-    }
-    if constexpr (A < D) element_rows_scatter<D, M, OPS, A + 1>(a, g, sw, tm, sb, F, FS);
-}
-
-// Tile numeric kernel (K1 + K2 + K4), the production path.
-//
-// One warp owns one tile (R = 32/L consecutive node rows, L lanes per row);
-// warps never synchronise with each other, so the SM overlaps one warp's
-// loads with another's arithmetic.
-//   phase 1  lanes over the tile's distinct elements: loads for two elements
-//            in flight, geometry once per element, then each local row the
-//            tile needs, scattered into the tile's entry-major fold array in
-//            warp-private shared memory;
-//   phase 2  each row's L lanes sum their entries' contiguous runs in
-//            registers (ascending element order) into an output segment;
-//   phase 3  the tile's rows are consecutive, so their CSR segment is one
-//            contiguous range: coalesced stores.
-// Every entry is the left-to-right sum of its contributions in ascending
-// element index: bitwise the reference's optv2 value.
-struct TileArgs {
-    const uint32_t *tile_e0;   // (ntiles) smallest element of each tile
-    const uint32_t *tile_tm;   // (ntiles) template id
-    const uint32_t *tm_off;    // (ntemplates) word offset of each template
-    const uint32_t *tm;        // template words
-    int max_inc;               // max incidences (slots) in one tile
-    int max_ent;               // max node-level entries in one tile
-};
-
-// Kernel choice: the row-gather kernel is the default (fastest measured on
-// every BASELINE config so far); SA_KERNEL=tile selects the tile kernel, whose
-// templates are then built in the symbolic phase.
-inline bool want_tile_kernel()
-{
-    const char *k = getenv("SA_KERNEL");
-    return k && strcmp(k, "tile") == 0;
-}
-// SA_KERNEL=chunk selects the element-chunk kernel (its symbolic data is then
-// built); the row-gather kernel is the default (fastest measured, profiles/)
-inline bool want_chunk_kernel()
-{
-    const char *k = getenv("SA_KERNEL");
-    return k && strcmp(k, "chunk") == 0;
-}
-
-// lanes per row (R = 32/L rows per warp tile): default per (d, m), override
-// with SA_TILE_LANES at plan creation (tuning).
-inline int default_lanes(int d, int m)
-{
-    return d == 1 ? 1 : (m == 1 ? (d == 2 ? 2 : 4) : (d == 2 ? 4 : 16));
-}
-inline int tile_lanes(int d, int m)
-{
-    const char *v = getenv("SA_TILE_LANES");
-    int L = v ? atoi(v) : default_lanes(d, m);
-    if (L != 1 && L != 2 && L != 4 && L != 8 && L != 16) L = default_lanes(d, m);
-    return L;
-}
-
-template <int D, int M, int OPS, int CORE, int L>
-__global__ void __launch_bounds__(128) k_numeric_tiles(NumArgs a, TileArgs t)
-{
-    constexpr int NOUT = n_outputs<OPS>();
-    constexpr int MM = M * M;
-    constexpr int R = 32 / L;
-    constexpr int WARPS = 4;
-    extern __shared__ __align__(16) double smem_d[];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t T = (int64_t)blockIdx.x * WARPS + wid;
-    const int64_t r0 = T * R;
-    if (r0 >= a.nnodes) return;
-    const int FS = (D + 1) * t.max_inc;          // fold positions per output
-    const int OS = M > 1 ? MM * t.max_ent : 0;   // output staging (vector case only)
-    double *F = smem_d + (size_t)wid * NOUT * ((size_t)FS * MM + OS);
-    double *outs = F + (size_t)NOUT * FS * MM;
-
-    const unsigned to = __ldg(t.tm_off + __ldg(t.tile_tm + T));
-    const unsigned eb = __ldg(t.tile_e0 + T);
-    const unsigned hdr = __ldg(t.tm + to);
-    const int ne = hdr & 0xff, nr = (hdr >> 8) & 0xff, NI = hdr >> 16;
-    const int NE = __ldg(t.tm + to + 1);
-    const unsigned SB = to + 2 + 2 * ne, PB = SB + 2 * NI, OB = PB + nr;
-
-    // phase 1: each distinct element once, two per lane in flight
-    int64_t emin = INT64_MAX;
-    for (int j = lane; j < ne; j += 64) {
-        const bool two = j + 32 < ne;
-        const int64_t e1 = (int64_t)eb + __ldg(t.tm + to + 2 + j);
-        const unsigned sw1 = __ldg(t.tm + to + 2 + ne + j);
-        const int64_t e2 = two ? (int64_t)eb + __ldg(t.tm + to + 2 + j + 32) : e1;
-        const unsigned sw2 = two ? __ldg(t.tm + to + 2 + ne + j + 32) : 0xffffffffu;
-        ElemRaw<D> x1, x2;
-        element_load1<D, OPS>(a, e1, x1);
-        element_load1<D, OPS>(a, e2, x2);
-        element_load2<D, OPS>(a, x1);
-        element_load2<D, OPS>(a, x2);
-        ElemGeo<D> g;
-        if (element_compute<D, OPS, CORE>(x1, g)) emin = min(emin, e1);
-        element_rows_scatter<D, M, OPS>(a, g, sw1, t.tm, SB, F, FS);
-        if (two) {
-            if (element_compute<D, OPS, CORE>(x2, g)) emin = min(emin, e2);
-            element_rows_scatter<D, M, OPS>(a, g, sw2, t.tm, SB, F, FS);
-        }
-    }
-    if (emin != INT64_MAX) atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)emin);
-    __syncwarp();
-
-    int nz[NOUT];
-#pragma unroll
-    for (int o = 0; o < NOUT; ++o) nz[o] = 0;
-    const int64_t base = a.indptr[(int64_t)M * r0];
-    if constexpr (M == 1) {
-        // phase 2 (scalar): the tile's entries are in CSR order and their runs
-        // are contiguous in the fold array; lane l sums the entries whose runs
-        // start in its 1/32 of the contributions (balanced, no carries: each
-        // run is summed left to right by one lane) and stores each result to
-        // its CSR position.
-        const unsigned LB = OB + ((NE + 2) >> 1);
-        const int kb = (__ldg(t.tm + LB + (lane >> 1)) >> (16 * (lane & 1))) & 0xffff;
-        const int ke = (__ldg(t.tm + LB + ((lane + 1) >> 1)) >> (16 * ((lane + 1) & 1))) & 0xffff;
-        if (kb < ke) {
-            auto off = [&](int k) { return (int)((__ldg(t.tm + OB + (k >> 1)) >> (16 * (k & 1))) & 0xffff); };
-            int k = kb;
-            int s = off(kb), next = off(kb + 1);
-            const int se = off(ke);
-            double acc[NOUT];
-#pragma unroll
-            for (int o = 0; o < NOUT; ++o) acc[o] = 0.0;
-            for (; s < se; ++s) {
-#pragma unroll
-                for (int o = 0; o < NOUT; ++o) acc[o] = SA_ADD(acc[o], F[o * FS + s]);
-                if (s + 1 == next) {
-#pragma unroll
-                    for (int o = 0; o < NOUT; ++o) {
-                        a.vals[o][base + k] = acc[o];
-                        nz[o] += (acc[o] == 0.0);
-                        acc[o] = 0.0;
-                    }
-                    ++k;
-                    if (k < ke) next = off(k + 1);
-                }
-            }
-        }
-    } else {
-        // phase 2 (vector): each row's L lanes sum their entries' runs
-        const int row = lane / L, jl = lane % L;
-        if (row < nr) {
-            const unsigned rw = __ldg(t.tm + PB + row);
-            const int deg = rw & 0xffff, entb = rw >> 16;
-            for (int k = jl; k < deg; k += L) {
-                const int kg = entb + k;
-                const unsigned s0 = (__ldg(t.tm + OB + (kg >> 1)) >> (16 * (kg & 1))) & 0xffff;
-                const unsigned s1 = (__ldg(t.tm + OB + ((kg + 1) >> 1)) >> (16 * ((kg + 1) & 1))) & 0xffff;
-#pragma unroll
-                for (int o = 0; o < NOUT; ++o) {
-                    double acc[MM];
-#pragma unroll
-                    for (int i = 0; i < MM; ++i) acc[i] = 0.0;
-                    const double *src = F + (size_t)o * FS * MM;
-                    for (unsigned s = s0; s < s1; ++s)
-#pragma unroll
-                        for (int i = 0; i < MM; ++i) acc[i] = SA_ADD(acc[i], src[s * MM + i]);
-                    double *orow = outs + o * OS + MM * entb;
-#pragma unroll
-                    for (int l = 0; l < M; ++l)
-#pragma unroll
-                        for (int n = 0; n < M; ++n) orow[l * M * deg + k * M + n] = acc[l * M + n];
-                }
-            }
-        }
-        __syncwarp();
-        // phase 3: the tile's CSR segment is contiguous -> coalesced stores
-#pragma unroll
-        for (int o = 0; o < NOUT; ++o) {
-            double *dst = a.vals[o] + base;
-            const double *src = outs + o * OS;
-            for (int i = lane; i < MM * NE; i += 32) {
-                const double v = src[i];
-                dst[i] = v;
-                nz[o] += (v == 0.0);
-            }
-        }
-    }
-#pragma unroll
-    for (int o = 0; o < NOUT; ++o) {
-        int v = nz[o];
-#pragma unroll
-        for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
-        if (lane == 0 && v) atomicAdd((unsigned long long *)(a.counters + o), (unsigned long long)v);
-    }
-}
-
-#include "sa_chunk.cuh"
 
 // compaction (K5): drop exact-zero entries (sparse.py:108-111)
 __global__ void k_row_nonzeros(const int64_t *__restrict__ indptr, const double *__restrict__ vals, int64_t nrows,
@@ -1920,259 +1565,6 @@ int mesh_coords(sa_mesh *M, const double *q, const double *vols, cudaStream_t st
     return SA_OK;
 }
 
-// Host side of the tile-template dedupe: build every tile in scratch, dedupe
-// by 64-bit signature, pack one copy per template, then verify every tile
-// word for word against its template (a hash collision disables templates).
-template <int D>
-int build_tile_templates(sa_plan *P, int R, cudaStream_t st)
-{
-    const int64_t nn = P->nnodes;
-    const int64_t ntiles = (nn + R - 1) / R;
-    int c = 0;
-    while ((1 << c) < R) ++c;
-    const int64_t NI = P->tile_max_inc[c], NE = P->tile_max_ent[c];
-    if (NI > 254) return SA_OK;  // tiles too wide for 8-bit slots: row-gather kernel
-    const int64_t stride64 = tile_stride_bound(NI, NE, R);
-    const int stride = (int)stride64;
-    uint32_t *scratch = nullptr, *words = nullptr;
-    uint64_t *sig = nullptr;
-    SA_CUDA_TRY(cudaMallocAsync((void **)&scratch, ntiles * stride64 * sizeof(uint32_t), st));
-    SA_CUDA_TRY(cudaMallocAsync((void **)&words, ntiles * sizeof(uint32_t), st));
-    SA_CUDA_TRY(cudaMallocAsync((void **)&sig, ntiles * sizeof(uint64_t), st));
-    SA_CUDA_TRY(cudaMallocAsync((void **)&P->tile_e0, ntiles * sizeof(uint32_t), st));
-    SA_CUDA_TRY(cudaMallocAsync((void **)&P->tile_tm, ntiles * sizeof(uint32_t), st));
-    SA_CUDA_TRY(cudaMemsetAsync(P->counters + 6, 0, sizeof(int64_t), st));
-    SA_LAUNCH(k_tile_build<D>, grid_for(ntiles, 64), 64, 0, st, P->inc_ptr, P->inc_e, P->fold, P->colptr, nn, R,
-              ntiles, stride, scratch, words, sig, P->tile_e0, (unsigned long long *)(P->counters + 6));
-    std::vector<uint64_t> hs(ntiles);
-    std::vector<uint32_t> hw(ntiles);
-    int64_t fail = 0;
-    SA_CUDA_TRY(cudaMemcpyAsync(hs.data(), sig, ntiles * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-    SA_CUDA_TRY(cudaMemcpyAsync(hw.data(), words, ntiles * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    SA_CUDA_TRY(cudaMemcpyAsync(&fail, P->counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SA_CUDA_TRY(cudaStreamSynchronize(st));
-    int rc = SA_OK;
-    if (!fail) {
-        std::unordered_map<uint64_t, uint32_t> ids;
-        std::vector<uint32_t> ttm(ntiles), off;
-        std::vector<int64_t> rep;
-        uint64_t total = 0;
-        for (int64_t i = 0; i < ntiles; ++i) {
-            auto it = ids.find(hs[i]);
-            if (it == ids.end()) {
-                const uint32_t id = (uint32_t)rep.size();
-                ids.emplace(hs[i], id);
-                rep.push_back(i);
-                off.push_back((uint32_t)total);
-                total += hw[i];
-                ttm[i] = id;
-            } else {
-                ttm[i] = it->second;
-            }
-        }
-        if (total < ((uint64_t)1 << 32)) {
-            P->n_templates = (int64_t)rep.size();
-            P->tm_nwords = (int64_t)total;
-            P->tile_rows = R;
-            int64_t *drep = nullptr;
-            SA_CUDA_TRY(cudaMallocAsync((void **)&drep, rep.size() * sizeof(int64_t), st));
-            SA_CUDA_TRY(cudaMallocAsync((void **)&P->tm_off, off.size() * sizeof(uint32_t), st));
-            SA_CUDA_TRY(cudaMallocAsync((void **)&P->tm, std::max<uint64_t>(total, 1) * sizeof(uint32_t), st));
-            SA_CUDA_TRY(cudaMemcpyAsync(drep, rep.data(), rep.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-            SA_CUDA_TRY(cudaMemcpyAsync(P->tm_off, off.data(), off.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-            SA_CUDA_TRY(cudaMemcpyAsync(P->tile_tm, ttm.data(), ntiles * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-            SA_LAUNCH(k_tile_pack, grid_for((int64_t)rep.size() * 32, 128), 128, 0, st, drep, (int64_t)rep.size(),
-                      scratch, stride, words, P->tm_off, P->tm);
-            SA_CUDA_TRY(cudaMemsetAsync(P->counters + 6, 0, sizeof(int64_t), st));
-            SA_LAUNCH(k_tile_verify, grid_for(ntiles * 32, 128), 128, 0, st, scratch, stride, words, ntiles,
-                      P->tile_tm, P->tm_off, P->tm, (unsigned long long *)(P->counters + 6));
-            int64_t bad = 0;
-            SA_CUDA_TRY(cudaMemcpyAsync(&bad, P->counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-            SA_CUDA_TRY(cudaStreamSynchronize(st));
-            SA_CUDA_TRY(cudaFreeAsync(drep, st));
-            P->tm_ok = (bad == 0);
-        }
-    }
-    SA_CUDA_TRY(cudaFreeAsync(scratch, st));
-    SA_CUDA_TRY(cudaFreeAsync(words, st));
-    SA_CUDA_TRY(cudaFreeAsync(sig, st));
-    return rc;
-}
-
-// Host side of the chunk kernel's symbolic data (see sa_chunk.cuh).
-template <int D>
-int build_chunks(sa_plan *P, cudaStream_t st)
-{
-    const int64_t nn = P->nnodes;
-    if (!nn || !P->n_inc) return SA_OK;
-    unsigned *mm = nullptr;
-    SA_CUDA_TRY(cudaMallocAsync((void **)&mm, 2 * sizeof(unsigned), st));
-    const unsigned init[2] = {0xffffffffu, 0u};
-    SA_CUDA_TRY(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, st));
-    SA_LAUNCH(k_inc_minmax<D>, std::min<int64_t>(grid_for(P->n_inc, 256), 148 * 8), 256, 0, st, P->inc_e, P->n_inc, mm);
-    unsigned hmm[2];
-    SA_CUDA_TRY(cudaMemcpyAsync(hmm, mm, sizeof hmm, cudaMemcpyDeviceToHost, st));
-    SA_CUDA_TRY(cudaStreamSynchronize(st));
-    SA_CUDA_TRY(cudaFreeAsync(mm, st));
-    const int C = chunk_elems(D, P->m);
-    const int64_t nchunks = ((int64_t)hmm[1] - hmm[0]) / C + 1;
-    P->ck_emin = hmm[0];
-    P->ck_emax = hmm[1];
-    P->ck_C = C;
-    P->ck_nchunks = nchunks;
-
-    // records: count, scan, fill
-    int64_t *rcount = nullptr, *rstart = nullptr;
-    SA_CUDA_TRY(cudaMallocAsync((void **)&rcount, (nn + 1) * sizeof(int64_t), st));
-    SA_CUDA_TRY(cudaMallocAsync((void **)&rstart, (nn + 1) * sizeof(int64_t), st));
-    SA_LAUNCH(k_chunk_records<D>, grid_for(nn, 128), 128, 0, st, P->inc_ptr, P->inc_e, P->fold, P->colptr, P->indptr,
-              nn, P->m, hmm[0], C, rcount, (const int64_t *)nullptr, (uint64_t *)nullptr, (uint32_t *)nullptr,
-              (uint32_t *)nullptr, (uint32_t *)nullptr, (uint32_t *)nullptr, (uint32_t *)nullptr, (uint16_t *)nullptr);
-    SA_TRY(exclusive_scan_i64(rcount, rstart, nn, P->scan_tmp, st));
-    int64_t nrec = 0;
-    SA_CUDA_TRY(cudaMemcpyAsync(&nrec, rstart + nn, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SA_CUDA_TRY(cudaStreamSynchronize(st));
-    if (nrec >= ((int64_t)1 << 32)) {
-        SA_CUDA_TRY(cudaFreeAsync(rcount, st));
-        SA_CUDA_TRY(cudaFreeAsync(rstart, st));
-        return SA_OK;
-    }
-    uint64_t *k0 = nullptr, *k1 = nullptr;
-    uint32_t *v0 = nullptr, *v1 = nullptr, *rp = nullptr, *rmeta = nullptr, *rprev = nullptr, *rcoff = nullptr;
-    uint16_t *contrib = nullptr;
-    const int64_t nr1 = std::max<int64_t>(nrec, 1);
-    SA_CUDA_TRY(cudaMallocAsync((void **)&k0, nr1 * sizeof(uint64_t), st));
-    SA_CUDA_TRY(cudaMallocAsync((void **)&k1, nr1 * sizeof(uint64_t), st));
-    SA_CUDA_TRY(cudaMallocAsync((void **)&v0, nr1 * sizeof(uint32_t), st));
-    SA_CUDA_TRY(cudaMallocAsync((void **)&v1, nr1 * sizeof(uint32_t), st));
-    SA_CUDA_TRY(cudaMallocAsync((void **)&rp, nr1 * sizeof(uint32_t), st));
-    SA_CUDA_TRY(cudaMallocAsync((void **)&rmeta, nr1 * sizeof(uint32_t), st));
-    SA_CUDA_TRY(cudaMallocAsync((void **)&rprev, nr1 * sizeof(uint32_t), st));
-    SA_CUDA_TRY(cudaMallocAsync((void **)&rcoff, nr1 * sizeof(uint32_t), st));
-    SA_CUDA_TRY(cudaMallocAsync((void **)&contrib, (D + 1) * P->n_inc * sizeof(uint16_t), st));
-    SA_LAUNCH(k_chunk_records<D>, grid_for(nn, 128), 128, 0, st, P->inc_ptr, P->inc_e, P->fold, P->colptr, P->indptr,
-              nn, P->m, hmm[0], C, (int64_t *)nullptr, (const int64_t *)rstart, k0, v0, rp, rmeta, rprev, rcoff,
-              contrib);
-    int kbits = 0;
-    while (((int64_t)1 << kbits) < nchunks) ++kbits;
-    int which = 0;
-    SA_TRY(radix::sort_pairs(k0, v0, k1, v1, nrec, std::max(8, (kbits + 7) & ~7), st, &which));
-    const uint64_t *skey = which ? k1 : k0;
-    const uint32_t *order = which ? v1 : v0;
-    int64_t *cstart = nullptr;
-    SA_CUDA_TRY(cudaMallocAsync((void **)&cstart, (nchunks + 1) * sizeof(int64_t), st));
-    SA_LAUNCH(k_chunk_bounds, grid_for(nrec, 256), 256, 0, st, skey, nrec, nchunks, cstart);
-    std::vector<int64_t> hcs(nchunks + 1);
-    SA_CUDA_TRY(cudaMemcpyAsync(hcs.data(), cstart, (nchunks + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SA_CUDA_TRY(cudaStreamSynchronize(st));
-    int64_t maxrec = 0;
-    for (int64_t k = 0; k < nchunks; ++k) maxrec = std::max(maxrec, hcs[k + 1] - hcs[k]);
-    const int64_t stride = 2 + 5 * maxrec + (int64_t)C * (D + 1) * (D + 1) / 2 + 8;
-    uint32_t *inv = nullptr;
-    SA_CUDA_TRY(cudaMallocAsync((void **)&inv, nr1 * sizeof(uint32_t), st));
-    SA_LAUNCH(k_inverse, grid_for(nrec, 256), 256, 0, st, order, nrec, inv);
-    uint32_t *fpos = nullptr;
-    SA_CUDA_TRY(cudaMallocAsync((void **)&fpos, nr1 * sizeof(uint32_t), st));
-    SA_LAUNCH(k_chunk_order, grid_for(nchunks, 128), 128, 0, st, (const int64_t *)cstart, nchunks, order, rmeta, fpos);
-
-    // templates, built and deduplicated in batches of chunks (bounded scratch)
-    SA_CUDA_TRY(cudaMallocAsync((void **)&P->ck_tm, nchunks * sizeof(uint32_t), st));
-    SA_CUDA_TRY(cudaMallocAsync((void **)&P->ck_pb, nchunks * sizeof(uint32_t), st));
-    const int64_t batch = std::max<int64_t>(1, std::min<int64_t>(nchunks, ((int64_t)1 << 29) / (stride * 4)));
-    uint32_t *scratch = nullptr, *words = nullptr;
-    uint64_t *sig = nullptr;
-    SA_CUDA_TRY(cudaMallocAsync((void **)&scratch, batch * stride * sizeof(uint32_t), st));
-    SA_CUDA_TRY(cudaMallocAsync((void **)&words, batch * sizeof(uint32_t), st));
-    SA_CUDA_TRY(cudaMallocAsync((void **)&sig, batch * sizeof(uint64_t), st));
-    std::unordered_map<uint64_t, uint32_t> ids;
-    std::vector<uint32_t> tm_off_h;
-    std::vector<uint32_t> tm_h;        // packed template words (host copy)
-    std::vector<uint32_t> ctm(nchunks);
-    std::vector<uint64_t> hs(batch);
-    std::vector<uint32_t> hw(batch);
-    bool ok = true;
-    for (int64_t b0 = 0; b0 < nchunks && ok; b0 += batch) {
-        const int64_t nb = std::min(batch, nchunks - b0);
-        SA_CUDA_TRY(cudaMemsetAsync(P->counters + 6, 0, sizeof(int64_t), st));
-        SA_LAUNCH(k_chunk_build, grid_for(nb, 64), 64, 0, st, (const int64_t *)cstart, b0, nb, order, inv, skey, rp,
-                  rmeta, rcoff, contrib, (const uint32_t *)fpos, stride, scratch, words, sig, P->ck_pb + b0,
-                  (unsigned long long *)(P->counters + 6));
-        int64_t fail = 0;
-        SA_CUDA_TRY(cudaMemcpyAsync(hs.data(), sig, nb * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaMemcpyAsync(hw.data(), words, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaMemcpyAsync(&fail, P->counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
-        if (fail) { ok = false; break; }
-        // new templates of this batch: copy their words back (small for structured meshes)
-        std::vector<int64_t> fresh;
-        for (int64_t i = 0; i < nb; ++i) {
-            auto it = ids.find(hs[i]);
-            if (it == ids.end()) {
-                const uint32_t id = (uint32_t)tm_off_h.size();
-                ids.emplace(hs[i], id);
-                tm_off_h.push_back((uint32_t)tm_h.size());
-                const size_t at = tm_h.size();
-                tm_h.resize(at + hw[i]);
-                SA_CUDA_TRY(cudaMemcpyAsync(tm_h.data() + at, scratch + i * stride, hw[i] * sizeof(uint32_t),
-                                            cudaMemcpyDeviceToHost, st));
-                ctm[b0 + i] = id;
-            } else {
-                ctm[b0 + i] = it->second;
-            }
-        }
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
-        // exact verification of this batch against the templates so far
-        if (tm_h.size() >= ((size_t)1 << 31)) { ok = false; break; }
-        uint32_t *dtm = nullptr, *doff = nullptr, *dctm = nullptr;
-        SA_CUDA_TRY(cudaMallocAsync((void **)&dtm, std::max<size_t>(tm_h.size(), 1) * sizeof(uint32_t), st));
-        SA_CUDA_TRY(cudaMallocAsync((void **)&doff, tm_off_h.size() * sizeof(uint32_t), st));
-        SA_CUDA_TRY(cudaMallocAsync((void **)&dctm, nb * sizeof(uint32_t), st));
-        SA_CUDA_TRY(cudaMemcpyAsync(dtm, tm_h.data(), tm_h.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-        SA_CUDA_TRY(cudaMemcpyAsync(doff, tm_off_h.data(), tm_off_h.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-        SA_CUDA_TRY(cudaMemcpyAsync(dctm, ctm.data() + b0, nb * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-        SA_CUDA_TRY(cudaMemsetAsync(P->counters + 6, 0, sizeof(int64_t), st));
-        SA_LAUNCH(k_tile_verify, grid_for(nb * 32, 128), 128, 0, st, scratch, (int)stride, words, nb, dctm, doff, dtm,
-                  (unsigned long long *)(P->counters + 6));
-        int64_t bad = 0;
-        SA_CUDA_TRY(cudaMemcpyAsync(&bad, P->counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
-        SA_CUDA_TRY(cudaFreeAsync(dtm, st));
-        SA_CUDA_TRY(cudaFreeAsync(doff, st));
-        SA_CUDA_TRY(cudaFreeAsync(dctm, st));
-        if (bad) ok = false;
-    }
-    if (ok) {
-        for (size_t t = 0; t < tm_off_h.size(); ++t) {
-            const size_t end = t + 1 < tm_off_h.size() ? tm_off_h[t + 1] : tm_h.size();
-            P->ck_maxw = std::max<int64_t>(P->ck_maxw, (int64_t)(end - tm_off_h[t]));
-        }
-        tm_off_h.push_back((uint32_t)tm_h.size());   // sentinel: template t spans [off[t], off[t+1])
-        P->ck_ntemplates = (int64_t)tm_off_h.size() - 1;
-        P->ck_nwords = (int64_t)tm_h.size();
-        SA_CUDA_TRY(cudaMallocAsync((void **)&P->ck_tm_off, std::max<size_t>(tm_off_h.size(), 1) * sizeof(uint32_t), st));
-        SA_CUDA_TRY(cudaMallocAsync((void **)&P->ck_tmw, std::max<size_t>(tm_h.size(), 1) * sizeof(uint32_t), st));
-        SA_CUDA_TRY(cudaMallocAsync((void **)&P->ck_flags, (nrec + 1) * sizeof(unsigned), st));
-        SA_CUDA_TRY(cudaMemsetAsync(P->ck_flags, 0, (nrec + 1) * sizeof(unsigned), st));
-        std::vector<uint32_t> rs(nchunks);
-        for (int64_t k = 0; k < nchunks; ++k) rs[k] = (uint32_t)hcs[k];
-        SA_CUDA_TRY(cudaMallocAsync((void **)&P->ck_rs, nchunks * sizeof(uint32_t), st));
-        SA_CUDA_TRY(cudaMemcpyAsync(P->ck_rs, rs.data(), nchunks * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-        P->ck_nrec = nrec;
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
-        SA_CUDA_TRY(cudaMemcpyAsync(P->ck_tm_off, tm_off_h.data(), tm_off_h.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-        SA_CUDA_TRY(cudaMemcpyAsync(P->ck_tmw, tm_h.data(), tm_h.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-        SA_CUDA_TRY(cudaMemcpyAsync(P->ck_tm, ctm.data(), nchunks * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-    }
-    SA_CUDA_TRY(cudaStreamSynchronize(st));
-    for (void *p : {(void *)rcount, (void *)rstart, (void *)k0, (void *)k1, (void *)v0, (void *)v1, (void *)rp,
-                    (void *)rmeta, (void *)rprev, (void *)rcoff, (void *)contrib, (void *)cstart, (void *)scratch,
-                    (void *)words, (void *)sig, (void *)inv, (void *)fpos})
-        SA_CUDA_TRY(cudaFreeAsync(p, st));
-    SA_CUDA_TRY(cudaStreamSynchronize(st));
-    P->ck_ok = ok;
-    return SA_OK;
-}
-
 template <int D>
 int symbolic_kernels(sa_plan *P, cudaStream_t st)
 {
@@ -2202,10 +1594,10 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
     // (max incidences <= NS_CAPI, checked here; neighbours <= NS_CAPC,
     // checked by the pass itself), else the general kernels
     bool fast = false;
-    const char *ns_s = getenv("SA_SYMFAST");
+
     // (default in 3D: measured warm C3 12.5 -> 9.9 ms, C5 65 -> 52 ms; in 2D
     // the general kernels are faster, C2 1.29 vs 1.71 ms)
-    if (nn && (ns_s ? atoi(ns_s) != 0 : D == 3)) {
+    if (nn && tune_int("symfast", D == 3) != 0) {
         SA_CUDA_TRY(cudaMemsetAsync(P->counters + 6, 0, 2 * sizeof(int64_t), st));
         SA_LAUNCH(k_max_diff, std::min<int64_t>(grid_for(nn, 256), 148 * 8), 256, 0, st, P->inc_ptr, nn,
                   (unsigned long long *)(P->counters + 6));
@@ -2257,10 +1649,10 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
     // warp-interleaved records for the row-gather kernel: on by default in 3D
     // (they replace three dependent gathers per incidence; measured faster),
     // off in 1D/2D (same speed there, 4x the record traffic); SA_WINC=0|1
-    const char *wi_s = getenv("SA_WINC");
+
     // (the records carry the volume: without it yet -- a mesh created
     // without coordinates or volumes -- the plan uses the 8-byte records)
-    const bool want_winc = (wi_s ? atoi(wi_s) != 0 : D == 3) && M->vols_ready;
+    const bool want_winc = tune_int("winc", D == 3) != 0 && M->vols_ready;
     if (nn && want_winc) {
         const int64_t nw = (nn + 31) / 32;
         SA_CUDA_TRY(cudaMallocAsync((void **)&P->wseg, (nw + 1) * sizeof(int64_t), st));
@@ -2274,35 +1666,6 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
         SA_LAUNCH(k_winc_fill<D>, grid_for(nn, 128), 128, 0, st, (const I *)M->me, M->vols, P->inc_ptr, P->inc, nn,
                   P->wseg, P->winc);
     }
-    // fold programs + templates: only for the tile / chunk kernels
-    if (want_tile_kernel() || want_chunk_kernel()) {
-        std::vector<int64_t> hcp(nn + 1), hip(nn + 1);
-        SA_CUDA_TRY(cudaMemcpyAsync(hcp.data(), P->colptr, (nn + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaMemcpyAsync(hip.data(), P->inc_ptr, (nn + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaMallocAsync((void **)&P->inc_e, std::max<int64_t>(P->n_inc, 1) * sizeof(uint32_t), st));
-        SA_CUDA_TRY(cudaMallocAsync((void **)&P->fold, std::max<int64_t>((D + 1) * P->n_inc, 1) * sizeof(uint16_t), st));
-        SA_CUDA_TRY(cudaMemsetAsync(P->counters + 6, 0, sizeof(int64_t), st));
-        if (nn)
-            SA_LAUNCH(k_fold_lists<D>, grid_for(nn, 128), 128, 0, st, P->inc_ptr, P->inc, nn, P->colptr, P->inc_e,
-                      P->fold, (unsigned long long *)(P->counters + 6));
-        int64_t too_many = 0;
-        SA_CUDA_TRY(cudaMemcpyAsync(&too_many, P->counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
-        P->fold_ok = (too_many == 0);
-        for (int c = 0; c < 6; ++c) {
-            const int64_t R = (int64_t)1 << c;
-            int64_t mi = 0, mz = 0;
-            for (int64_t r0 = 0; r0 < nn; r0 += R) {
-                mi = std::max(mi, hip[std::min(nn, r0 + R)] - hip[r0]);
-                mz = std::max(mz, hcp[std::min(nn, r0 + R)] - hcp[r0]);
-            }
-            P->tile_max_inc[c] = mi;
-            P->tile_max_ent[c] = mz;
-        }
-        if (P->fold_ok && md <= 255 && nn && want_tile_kernel()) {
-            SA_TRY(build_tile_templates<D>(P, 32 / tile_lanes(D, P->m), st));
-        }
-    }
     const int m = P->m;
     P->nnz = (int64_t)m * m * P->n_colnodes;
     if (P->nnz >= ((int64_t)1 << 31) || (int64_t)m * M->nq >= ((int64_t)1 << 31))
@@ -2313,232 +1676,129 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
     SA_LAUNCH(k_dof_csr, grid_for(nn + 1, 128), 128, 0, st, P->colptr, P->cols, nn, m, P->indptr, P->indices);
     SA_CUDA_TRY(cudaFreeAsync(cnt, st));
     SA_CUDA_TRY(cudaStreamSynchronize(st));
-    if (P->fold_ok && want_chunk_kernel()) SA_TRY(build_chunks<D>(P, st));
     return SA_OK;
 }
 
-// Kernel selection: the tile kernel whenever the plan has verified fold
-// templates; SA_KERNEL=rowgather forces the v1 kernel (tests, comparison).
+// One-pass row gather.  Launch shape per operator (measured on the BASELINE
+// configs, profiles/r01/README.md): the kernel is latency-bound, so
+// occupancy wins over per-thread ILP except for the register-heavy elastic
+// operator, which gains from the 3-deep software pipeline; lean instances
+// (no nodal mass weight) drop the generic branches.
 template <int D, int M, int OPS, int CORE>
 int launch_rowgather(const NumArgs &a, int64_t nnodes, cudaStream_t st)
 {
     constexpr int NOUT = n_outputs<OPS>();
-    // SA_ILP (1|2|3): incidences in flight per thread (3 = software
-    // pipeline); SA_MINB (0|3|6|8): minimum resident 128-thread blocks per SM
-    // the single-incidence kernel is register-capped for (0 = no cap)
-    const char *ilp_s = getenv("SA_ILP"), *mb_s = getenv("SA_MINB");
-    // defaults measured on the BASELINE configs (profiles/r01): the kernel is
-    // latency-bound, so occupancy wins over per-thread ILP except for the
-    // register-heavy elastic operator, which gains from the pipeline
-    const int ilp = ilp_s ? atoi(ilp_s) : (M > 1 ? 3 : 1);
-    int minb = mb_s ? atoi(mb_s) : (M > 1 ? 0 : (OPS & OP_GENERAL) ? 3 : (D <= 2 ? 8 : 6));
-    // (2D, more than one wave of 8 blocks/SM: 10 blocks/SM at 48 registers
-    // beats 8 at 60 despite an 8-byte spill -- C2 0.299 -> 0.289 ms; a
-    // single wave (C1) keeps 8)
-
     const size_t per_thread = (size_t)NOUT * (a.acc_stride | 1) * sizeof(double);
     int block = 128;
     while (per_thread * block > 100 * 1024 && block > 32) block /= 2;
     const size_t smem = per_thread * block;
     if (smem > 200 * 1024)
         return set_error(SA_ERR_CAPACITY, "row accumulators need %zu B of shared memory per %d threads", smem, block);
+    const bool lean = !((OPS & OP_MASS) && a.w) && (a.winc != nullptr) == (D == 3);
     void (*kern)(NumArgs);
-    // lean instances (SA_LEAN=0 disables) when no diagnostics run and any mass
-    // weight is constant
-    const char *ln_s = getenv("SA_LEAN");
-    const bool lean = (ln_s ? atoi(ln_s) != 0 : true) && a.dbg == 0 && !((OPS & OP_MASS) && a.w) &&
-                      (a.winc != nullptr) == (D == 3);
-    if (!mb_s && lean && D <= 2 && M == 1 && !(OPS & OP_GENERAL) && nnodes > (int64_t)148 * 8 * 128) minb = 10;
-    if (ilp == 2) kern = k_numeric_rowgather<D, M, OPS, CORE, 2, 1>;
-    else if (ilp == 3) kern = lean ? k_numeric_rowgather<D, M, OPS, CORE, 3, 1, false, true>
-                                   : k_numeric_rowgather<D, M, OPS, CORE, 3, 1>;
-    else if (minb == 8) kern = lean ? k_numeric_rowgather<D, M, OPS, CORE, 1, 8, false, true>
-                                    : k_numeric_rowgather<D, M, OPS, CORE, 1, 8>;
-    else if (minb == 6) kern = lean ? k_numeric_rowgather<D, M, OPS, CORE, 1, 6, false, true>
-                                    : k_numeric_rowgather<D, M, OPS, CORE, 1, 6>;
-    else if (minb == 7 && lean && M == 1) kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 7, false, true>;
-    else if (minb == 10 && lean && M == 1) kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 10, false, true>;
-    else if (minb == 12 && lean && M == 1) kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 12, false, true>;
-    else if (minb == 3) kern = lean ? k_numeric_rowgather<D, M, OPS, CORE, 1, 3, false, true>
-                                    : k_numeric_rowgather<D, M, OPS, CORE, 1, 3>;
-    else kern = lean ? k_numeric_rowgather<D, M, OPS, CORE, 1, 1, false, true>
-                     : k_numeric_rowgather<D, M, OPS, CORE, 1, 1>;
+    if constexpr (M > 1) {
+        kern = lean ? k_numeric_rowgather<D, M, OPS, CORE, 3, 1, false, true> : k_numeric_rowgather<D, M, OPS, CORE, 3, 1>;
+    } else if constexpr ((OPS & OP_GENERAL) != 0) {
+        kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 3>;
+    } else if constexpr (D == 3) {
+        kern = lean ? k_numeric_rowgather<D, M, OPS, CORE, 1, 6, false, true> : k_numeric_rowgather<D, M, OPS, CORE, 1, 6>;
+    } else {
+        // 2D/1D: 10 blocks/SM at 48 registers beats 8 at 60 once the grid
+        // has more than one wave (C2 0.299 -> 0.289 ms); one wave keeps 8
+        if (lean && nnodes > (int64_t)148 * 8 * 128) kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 10, false, true>;
+        else if (lean) kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 8, false, true>;
+        else kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 8>;
+    }
     SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (nnodes) SA_LAUNCH(kern, grid_for(nnodes, block), block, smem, st, a);
     return SA_OK;
 }
 
-// returns SA_OK after launching, 1000 when the kernel's staging does not fit
-#define SA_TRY_OR_FALL(...)                  \
-    do {                                     \
-        int _r = (__VA_ARGS__);              \
-        if (_r == SA_OK) return SA_OK;       \
-        if (_r != 1000) return _r;           \
-    } while (0)
-
-template <int D, int M, int OPS, int CORE, int L>
-int launch_tiles(const sa_plan *P, const NumArgs &a, cudaStream_t st)
+// Fast general operator, guarded rows: recompute each flagged row in
+// reference order (bitwise element values, ascending element fold straight
+// into the row's CSR segment) and count its exact zeros (sparse.py:108-111).
+template <int D, int OPS, int CORE>
+__global__ void k_guard_fixup(NumArgs a)
 {
     constexpr int NOUT = n_outputs<OPS>();
-    constexpr int VPI = NOUT * M * M * (D + 1);
-    constexpr int R = 32 / L;
-    constexpr int LOG2R = R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : R == 8 ? 3 : R == 16 ? 4 : 5;
-    TileArgs t;
-    t.tile_e0 = P->tile_e0;
-    t.tile_tm = P->tile_tm;
-    t.tm_off = P->tm_off;
-    t.tm = P->tm;
-    t.max_inc = (int)P->tile_max_inc[LOG2R];
-    t.max_ent = (int)P->tile_max_ent[LOG2R];
-    const size_t warp_bytes =
-        (size_t)NOUT * ((size_t)(D + 1) * t.max_inc * M * M + (M > 1 ? (size_t)M * M * t.max_ent : 0)) * 8;
-    const size_t smem = 4 * warp_bytes;
-    if (smem > 200 * 1024) return 1000;
-    (void)VPI;
-    auto kern = k_numeric_tiles<D, M, OPS, CORE, L>;
-    SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (P->nnodes) SA_LAUNCH(kern, grid_for(P->nnodes, 4 * R), 128, smem, st, a, t);
-    return SA_OK;
+    const int n = *a.nflag;
+    int nz[NOUT];
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) nz[o] = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t nl = a.flag_rows[i];
+        const int64_t base = a.indptr[nl];
+        const int deg = (int)(a.colptr[nl + 1] - a.colptr[nl]);
+        for (int o = 0; o < NOUT; ++o)
+            for (int k = 0; k < deg; ++k) a.vals[o][base + k] = 0.0;
+        for (int64_t t = a.inc_ptr[nl]; t < a.inc_ptr[nl + 1]; ++t) {
+            const uint2 rec = a.inc[t];
+            ElemRaw<D> x;
+            element_load1<D, OPS>(a, rec.x & 0x3fffffffu, x);
+            element_load2<D, OPS>(a, x);
+            ElemGeo<D> g;
+            element_compute<D, OPS, CORE>(x, g);
+            double vals[(D + 1) * NOUT];
+            krow_runtime<D, 1, OPS>(a, g, rec.x >> 30, vals);
+#pragma unroll
+            for (int b = 0; b <= D; ++b) {
+                const int rk = (rec.y >> (8 * b)) & 0xff;
+#pragma unroll
+                for (int o = 0; o < NOUT; ++o) a.vals[o][base + rk] += vals[b * NOUT + o];
+            }
+        }
+        for (int o = 0; o < NOUT; ++o)
+            for (int k = 0; k < deg; ++k) nz[o] += (a.vals[o][base + k] == 0.0);
+    }
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o)
+        if (nz[o]) atomicAdd((unsigned long long *)(a.counters + o), (unsigned long long)nz[o]);
 }
 
-template <int D, int M, int OPS, int CORE>
-int launch_chunks(const sa_plan *P, const NumArgs &a, cudaStream_t st)
-{
-    constexpr int NOUT = n_outputs<OPS>();
-    constexpr int VPE = NOUT * M * M * (D + 1) * (D + 1);
-    const size_t smem = (size_t)P->ck_C * VPE * sizeof(double) + (size_t)P->ck_maxw * sizeof(uint32_t);
-    if (smem > 200 * 1024) return 1000;
-    auto kern = k_numeric_chunks<D, M, OPS, CORE>;
-    SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int dev = 0, nsm = 148, occ = 1;
-    SA_CUDA_TRY(cudaGetDevice(&dev));
-    SA_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    const int threads = std::max(64, std::min(256, P->ck_C));
-    SA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
-    ChunkArgs c;
-    c.chunk_tm = P->ck_tm;
-    c.chunk_pb = P->ck_pb;
-    c.tm_off = P->ck_tm_off;
-    c.tm = P->ck_tmw;
-    c.chunk_rs = P->ck_rs;
-    c.rflags = P->ck_flags;
-    c.ticket = P->ck_flags + P->ck_nrec;
-    c.epoch = ++const_cast<sa_plan *>(P)->ck_epoch;
-    c.nowait = getenv("SA_CHUNK_NOWAIT") != nullptr;
-    c.max_words = (int)P->ck_maxw;
-    c.nchunks = P->ck_nchunks;
-    c.emin = P->ck_emin;
-    c.emax = P->ck_emax;
-    c.C = P->ck_C;
-    SA_CUDA_TRY(cudaMemsetAsync(c.ticket, 0, sizeof(unsigned), st));
-    const int64_t grid = std::min<int64_t>(P->ck_nchunks, (int64_t)nsm * std::max(occ, 1));
-    if (grid > 0) SA_LAUNCH(kern, (unsigned)grid, threads, smem, st, a, c);
-    return SA_OK;
-}
-
-// the fold of the overlapped two-pass (ILP 2, 128 threads)
-template <int D, int M, int OPS, int CORE>
-auto fold_kernel() -> void (*)(NumArgs)
-{
-    return k_numeric_rowgather<D, M, OPS, CORE, 2, 1, true>;
-}
-template <int OPS>
-size_t fold_smem(const NumArgs &a)
-{
-    return (size_t)n_outputs<OPS>() * (a.acc_stride | 1) * sizeof(double) * 128;
-}
-
+// Two-pass numeric (3D general operator): element pass, then the ordered
+// fold.  Element pass: the persistent three-stage cp.async pipeline when
+// every batch's vertex records fit the stage (C5: 3 blocks/SM at 164
+// registers), else one thread per element with direct gathers.  Fast mode
+// (default for the general operator): fused-multiply-add local matrices in
+// the element pass, the zero guard in the fold, guarded rows recomputed.
 template <int D, int M, int OPS, int CORE>
 int launch_twopass(const sa_plan *P, const NumArgs &a, int64_t nnodes, cudaStream_t st)
 {
     constexpr int NOUT = n_outputs<OPS>();
-    // SA_EMINB (0|3|4): minimum resident 128-thread blocks per SM of the
-    // element pass (register cap)
-    const char *emb_s = getenv("SA_EMINB");
-    // (measured on C5: no cap 210 registers 11.8 ms, 3 blocks 8.6 ms, 4 blocks 9.0 ms)
-    const int eminb = emb_s ? atoi(emb_s) : 3;
-    bool batched = false;
-    if constexpr (OPS == OP_GENERAL && D == 3) {
-        if (a.eb_loc && a.gen_packed) {
-            // batched element pass (vertex records deduplicated per batch in smem)
-            batched = true;
-            const size_t smem = (size_t)std::max(a.eb_maxn, 1) * EB_REC * sizeof(double);
-            // SA_EMINB for the batched pass: 3 | 4 (default) | 5 blocks per SM
-            const int bm = emb_s ? atoi(emb_s) : 4;
-            const char *pp_s = getenv("SA_EPIPE");
-            const bool pipe = a.eb_allfit && (pp_s ? atoi(pp_s) != 0 : true);
-            if (pipe) {
-                // persistent, three-stage cp.async pipeline
-                // (C5: 3 blocks/SM at 164 registers 6.73 ms, 4 at 128 + spill 6.79,
-                // unpipelined batched 7.18)
-                const int pm = pp_s && atoi(pp_s) > 1 ? atoi(pp_s) : 3;
-                auto pk = pm == 3 ? k_element_rows_pipe<D, M, OPS, CORE, 3> : k_element_rows_pipe<D, M, OPS, CORE, 4>;
-                const size_t psm = 2 * (size_t)std::max(a.eb_maxn, 1) * EB_REC * sizeof(double) +
-                                   3 * (EB_CAP + 1) * sizeof(int);
-                SA_CUDA_TRY(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
-                int dev = 0, nsm = 148, occ = 0;
-                SA_CUDA_TRY(cudaGetDevice(&dev));
-                SA_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-                SA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pk, EB_SIZE, psm));
-                const int64_t nb = (a.ne + EB_SIZE - 1) / EB_SIZE;
-                const int K = (int)P->ov_bcut.size() - 1;
-                if (K >= 1 && P->ov_stream) {
-                    // element chunk k on st, then the fold of the rows whose
-                    // elements are all in chunks <= k on the second stream:
-                    // fold k (DRAM-bound) overlaps element chunk k+1 (fp64)
-                    auto fk = fold_kernel<D, M, OPS, CORE>();
-                    const size_t fsm = fold_smem<OPS>(a);
-                    SA_CUDA_TRY(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
-                    for (int k = 0; k < K; ++k) {
-                        NumArgs ak = a;
-                        ak.eb_b0 = P->ov_bcut[k];
-                        ak.eb_b1 = P->ov_bcut[k + 1];
-                        const unsigned g = (unsigned)std::min<int64_t>(std::max<int64_t>(ak.eb_b1 - ak.eb_b0, 1),
-                                                                       (int64_t)nsm * std::max(occ, 1));
-                        if (ak.eb_b1 > ak.eb_b0) SA_LAUNCH(pk, g, EB_SIZE, psm, st, ak);
-                        SA_CUDA_TRY(cudaEventRecord(P->ov_events[k], st));
-                        SA_CUDA_TRY(cudaStreamWaitEvent(P->ov_stream, P->ov_events[k], 0));
-                        ak.row0 = 32 * P->ov_wcut[k];
-                        ak.row1 = std::min<int64_t>(nnodes, 32 * P->ov_wcut[k + 1]);
-                        if (ak.row1 > ak.row0)
-                            SA_LAUNCH(fk, grid_for(ak.row1 - ak.row0, 128), 128, fsm, P->ov_stream, ak);
-                    }
-                    SA_CUDA_TRY(cudaEventRecord(P->ov_events[K], P->ov_stream));
-                    SA_CUDA_TRY(cudaStreamWaitEvent(st, P->ov_events[K], 0));
-                    return SA_OK;
-                }
-                const unsigned g = (unsigned)std::min<int64_t>(nb, (int64_t)nsm * std::max(occ, 1));
-                if (a.ne) SA_LAUNCH(pk, g, EB_SIZE, psm, st, a);
-            } else {
-                auto kern = bm == 3 ? k_element_rows_batched<D, M, OPS, CORE, 3>
-                            : bm == 5 ? k_element_rows_batched<D, M, OPS, CORE, 5>
-                            : a.eb_allfit ? k_element_rows_batched<D, M, OPS, CORE, 4, true>
-                                          : k_element_rows_batched<D, M, OPS, CORE, 4>;
-                SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                if (a.ne) SA_LAUNCH(kern, grid_for(a.ne, EB_SIZE), EB_SIZE, smem, st, a);
-            }
+    constexpr bool GEN3 = OPS == OP_GENERAL && D == 3 && M == 1;
+    const bool pipe = GEN3 && a.eb_loc && a.gen_packed && a.eb_allfit;
+    const bool fast = pipe && !a.exact;
+    if constexpr (GEN3) {
+        if (pipe) {
+            // (fast: 126 registers, 4 blocks/SM -- C5 7.89 vs 8.05 ms at 3)
+            auto pk = fast ? k_element_rows_pipe<D, M, OPS, CORE, 4, true> : k_element_rows_pipe<D, M, OPS, CORE, 3>;
+            const size_t psm = 2 * (size_t)std::max(a.eb_maxn, 1) * EB_REC * sizeof(double) +
+                               3 * (EB_CAP + 1) * sizeof(int);
+            SA_CUDA_TRY(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+            int dev = 0, nsm = 148, occ = 0;
+            SA_CUDA_TRY(cudaGetDevice(&dev));
+            SA_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+            SA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pk, EB_SIZE, psm));
+            const int64_t nb = (a.ne + EB_SIZE - 1) / EB_SIZE;
+            const unsigned g = (unsigned)std::min<int64_t>(nb, (int64_t)nsm * std::max(occ, 1));
+            if (a.ne) SA_LAUNCH(pk, g, EB_SIZE, psm, st, a);
         }
     }
-    if (batched) {
-    } else if (a.ne) {
-        if (eminb == 4) SA_LAUNCH((k_element_rows<D, M, OPS, CORE, 4>), grid_for(a.ne, 128), 128, 0, st, a);
-        else if (eminb == 3) SA_LAUNCH((k_element_rows<D, M, OPS, CORE, 3>), grid_for(a.ne, 128), 128, 0, st, a);
-        else SA_LAUNCH((k_element_rows<D, M, OPS, CORE, 1>), grid_for(a.ne, 128), 128, 0, st, a);
-    }
-    const char *ilp_s = getenv("SA_ILP");
-    const int ilp = ilp_s ? atoi(ilp_s) : 2;
+    if (!pipe && a.ne) SA_LAUNCH((k_element_rows<D, M, OPS, CORE, 3>), grid_for(a.ne, 128), 128, 0, st, a);
     const size_t per_thread = (size_t)NOUT * (a.acc_stride | 1) * sizeof(double);
     int block = 128;
     while (per_thread * block > 100 * 1024 && block > 32) block /= 2;
     const size_t smem = per_thread * block;
     if (smem > 200 * 1024)
         return set_error(SA_ERR_CAPACITY, "row accumulators need %zu B of shared memory per %d threads", smem, block);
-    void (*kern)(NumArgs);
-    if (ilp >= 4) kern = k_numeric_rowgather<D, M, OPS, CORE, 4, 1, true>;
-    else if (ilp == 2 || ilp == 3) kern = k_numeric_rowgather<D, M, OPS, CORE, 2, 1, true>;
-    else kern = k_numeric_rowgather<D, M, OPS, CORE, 1, 1, true>;
+    void (*kern)(NumArgs) = fast ? k_numeric_rowgather<D, M, OPS, CORE, 2, 1, true, false, true>
+                                 : k_numeric_rowgather<D, M, OPS, CORE, 2, 1, true>;
     SA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (fast) SA_CUDA_TRY(cudaMemsetAsync(a.nflag, 0, sizeof(int), st));
     if (nnodes) SA_LAUNCH(kern, grid_for(nnodes, block), block, smem, st, a);
+    if constexpr (M == 1) {
+        if (fast && nnodes) SA_LAUNCH((k_guard_fixup<D, OPS, CORE>), 148, 128, 0, st, a);
+    }
     return SA_OK;
 }
 
@@ -2546,21 +1806,7 @@ template <int D, int M, int OPS, int CORE>
 int launch_numeric(const sa_plan *P, const NumArgs &a, cudaStream_t st)
 {
     if (a.kbuf) return launch_twopass<D, M, OPS, CORE>(P, a, P->nnodes, st);
-    if (P->ck_ok && want_chunk_kernel()) SA_TRY_OR_FALL(launch_chunks<D, M, OPS, CORE>(P, a, st));
-
-    const int64_t nnodes = P->nnodes;
-    const bool use_tile = P->tm_ok && want_tile_kernel();
-    if (use_tile) {
-        switch (32 / P->tile_rows) {
-            case 1: SA_TRY_OR_FALL(launch_tiles<D, M, OPS, CORE, 1>(P, a, st)); break;
-            case 2: SA_TRY_OR_FALL(launch_tiles<D, M, OPS, CORE, 2>(P, a, st)); break;
-            case 4: SA_TRY_OR_FALL(launch_tiles<D, M, OPS, CORE, 4>(P, a, st)); break;
-            case 8: SA_TRY_OR_FALL(launch_tiles<D, M, OPS, CORE, 8>(P, a, st)); break;
-            case 16: SA_TRY_OR_FALL(launch_tiles<D, M, OPS, CORE, 16>(P, a, st)); break;
-            default: break;
-        }
-    }
-    return launch_rowgather<D, M, OPS, CORE>(a, nnodes, st);
+    return launch_rowgather<D, M, OPS, CORE>(a, P->nnodes, st);
 }
 
 template <int D, int M, int OPS>
@@ -2723,15 +1969,9 @@ int sa_mesh_destroy(sa_mesh *M)
 int sa_plan_destroy(sa_plan *P)
 {
     if (!P) return SA_OK;
-    if (P->ov_stream) {
-        cudaStreamSynchronize(P->ov_stream);
-        cudaStreamDestroy(P->ov_stream);
-    }
-    for (auto ev : P->ov_events) cudaEventDestroy(ev);
-    free_all({P->inc_ptr, P->inc, P->winc, P->wseg, P->colptr, P->cols, P->indptr, P->indices, P->counters, P->scan_tmp, P->inc_e,
-              P->fold, P->tile_e0, P->tile_tm, P->tm_off, P->tm, P->ck_tm, P->ck_pb, P->ck_tm_off, P->ck_tmw,
-              P->ck_flags, P->ck_rs, P->epos, P->kbuf, P->tp_rank, P->eb_verts,
-              P->eb_count, P->eb_loc});
+    free_all({P->inc_ptr, P->inc, P->winc, P->wseg, P->colptr, P->cols, P->indptr, P->indices, P->counters,
+              P->scan_tmp, P->epos, P->kbuf, P->tp_rank, P->eb_verts, P->eb_count, P->eb_loc, P->gd_flag_rows,
+              P->gd_nflag});
     delete P;
     return SA_OK;
 }
@@ -2783,10 +2023,9 @@ int sa_plan_info(const sa_plan *P, int64_t *nrows, int64_t *nnz, int64_t *max_ro
 int sa_plan_stats(const sa_plan *P, int64_t *out, int n)
 {
     if (!P || !out) return set_error(SA_ERR_ARG, "plan/out is NULL");
-    const int64_t v[12] = {P->n_templates, P->tm_ok ? 1 : 0, P->fold_ok ? 1 : 0, P->n_inc,
-                           P->tm_nwords, P->max_deg, P->nnodes, P->nnz,
-                           P->ck_ok ? 1 : 0, P->ck_nchunks, P->ck_ntemplates, P->ck_nwords};
-    for (int i = 0; i < n && i < 12; ++i) out[i] = v[i];
+    const int64_t v[8] = {P->n_inc, P->max_deg, P->nnodes, P->nnz, P->n_winc, P->tp_nslots, P->eb_allfit ? 1 : 0,
+                          P->eb_maxn};
+    for (int i = 0; i < n && i < 8; ++i) out[i] = v[i];
     return SA_OK;
 }
 
@@ -2801,13 +2040,15 @@ int sa_plan_pattern(const sa_plan *P, int64_t *indptr_dev, int32_t *indices_dev,
     return SA_OK;
 }
 
-// two-pass numeric ("element rows"): SA_KERNEL=twopass|rowgather forces it
-// on/off; by default it serves the operators where it measured faster
+// two-pass numeric ("element rows") serves the 3D general operator, where
+// recomputing each element once per vertex row costs more than the local-row
+// buffer (measured); SA_TUNE=kernel=twopass|rowgather forces
+// either path for any operator (tests, A/B)
 static bool want_twopass(int ops, int d, int m)
 {
-    const char *k = getenv("SA_KERNEL");
-    if (k && *k) return strcmp(k, "twopass") == 0;
     (void)m;
+    if (tune_is("kernel", "twopass")) return true;
+    if (tune_is("kernel", "rowgather")) return false;
     return ops == SA_OP_GENERAL && d == 3;
 }
 
@@ -2867,36 +2108,10 @@ static int ensure_twopass(sa_plan *P, int kstride, bool batches, cudaStream_t st
         SA_CUDA_TRY(cudaFreeAsync(mx, st));
         P->eb_maxn = (int)std::min<unsigned long long>(h, EB_CAP);
         P->eb_allfit = h <= EB_CAP;
-        // overlap chunks (opt-in SA_OVERLAP = K): batch cuts, and per chunk
-        // the warps whose rows' largest element lies before the chunk's end.
-        // Off by default: measured C5 9.03 ms without, 9.07 / 9.12 / 9.22 ms
-        // with K = 2 / 4 / 8 -- the element pass holds the whole register
-        // file (3 x 128 threads x 164), so fold blocks cannot co-reside
-        const char *ov_s = getenv("SA_OVERLAP");
-        const int K = ov_s ? atoi(ov_s) : 0;
-        const int64_t nn = P->nnodes, nw = (nn + 31) / 32;
-        if (K >= 2 && P->eb_allfit && nb >= 4 * K && nw > 0) {
-            unsigned *wm = nullptr;
-            SA_CUDA_TRY(cudaMallocAsync((void **)&wm, nw * sizeof(unsigned), st));
-            SA_LAUNCH(k_warp_emax, grid_for(nw, 128), 128, 0, st, P->inc_ptr, P->inc, nn, wm);
-            std::vector<unsigned> hw(nw);
-            SA_CUDA_TRY(cudaMemcpyAsync(hw.data(), wm, nw * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-            SA_CUDA_TRY(cudaStreamSynchronize(st));
-            SA_CUDA_TRY(cudaFreeAsync(wm, st));
-            P->ov_bcut.assign(K + 1, 0);
-            P->ov_wcut.assign(K + 1, 0);
-            for (int k = 0; k <= K; ++k) P->ov_bcut[k] = nb * k / K;
-            unsigned pm = 0;
-            int64_t w = 0;
-            for (int k = 0; k < K; ++k) {
-                const int64_t e_end = P->e_lo + std::min<int64_t>(P->ov_bcut[k + 1] * EB_SIZE, ne);
-                while (w < nw && (int64_t)std::max(pm, hw[w]) < e_end) pm = std::max(pm, hw[w++]);
-                P->ov_wcut[k + 1] = k + 1 == K ? nw : w;
-            }
-            SA_CUDA_TRY(cudaStreamCreateWithFlags(&P->ov_stream, cudaStreamNonBlocking));
-            P->ov_events.resize(K + 1);
-            for (auto &ev : P->ov_events) SA_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        }
+    }
+    if (!P->gd_nflag) {   // fast general operator: guarded-row list
+        SA_CUDA_TRY(cudaMallocAsync((void **)&P->gd_flag_rows, std::max<int64_t>(P->nnodes, 1) * sizeof(uint32_t), st));
+        SA_CUDA_TRY(cudaMallocAsync((void **)&P->gd_nflag, sizeof(int), st));
     }
     const int64_t kelems = (int64_t)kstride * P->tp_nslots;
     if (P->kbuf_elems < kelems) {
@@ -2910,11 +2125,7 @@ static int ensure_twopass(sa_plan *P, int kstride, bool batches, cudaStream_t st
     return SA_OK;
 }
 
-static bool want_batches(int ops, int d)
-{
-    const char *eb_s = getenv("SA_EBATCH");
-    return ops == SA_OP_GENERAL && d == 3 && (eb_s ? atoi(eb_s) != 0 : true);
-}
+static bool want_batches(int ops, int d) { return ops == SA_OP_GENERAL && d == 3; }
 
 static int plan_nout(int ops)
 {
@@ -2928,6 +2139,7 @@ int sa_plan_prepare(sa_plan *P, int ops, void *stream)
     if (!P) return set_error(SA_ERR_ARG, "plan is NULL");
     const int d = P->mesh->d;
     SA_TRY(set_device(P->mesh->device));
+    ops &= 15;
     if (want_twopass(ops, d, P->m) && P->n_inc < 0xffffffffLL) {
         const int ks = (d + 1) * plan_nout(ops) * P->m * P->m;
         SA_TRY(ensure_twopass(P, ks, want_batches(ops, d), (cudaStream_t)stream));
@@ -2947,12 +2159,12 @@ int sa_numeric(sa_plan *P, int ops, const sa_coeffs *cf, double *const *vals_dev
     cudaStream_t st = (cudaStream_t)stream;
     NumArgs a;
     memset(&a, 0, sizeof a);
+    a.exact = (ops & SA_OP_EXACT) ? 1 : 0;
+    ops &= 15;
+
     a.qv = M->qv; a.me = M->me; a.vols = M->vols;
     a.nnodes = P->nnodes; a.node_begin = P->node_begin;
     a.inc_ptr = P->inc_ptr; a.inc = P->inc; a.winc = P->winc; a.wseg = P->wseg; a.colptr = P->colptr; a.indptr = P->indptr; a.cols = P->cols;
-    a.dbg = getenv("SA_DBG") ? atoi(getenv("SA_DBG")) : 0;
-    a.row0 = 0;
-    a.row1 = P->nnodes;
     a.acc_stride = (int)(P->m * P->m * std::max<int64_t>(P->max_deg, 1));
     int nout = 0;
     for (int bit = 1; bit <= 8; bit <<= 1)
@@ -2965,6 +2177,9 @@ int sa_numeric(sa_plan *P, int ops, const sa_coeffs *cf, double *const *vals_dev
     a.lamb = cf->lamb; a.lamb_const = cf->lamb_const;
     a.mu = cf->mu; a.mu_const = cf->mu_const;
     a.A = cf->A; a.b = cf->b; a.c = cf->c; a.a0 = cf->a0; a.gen_packed = cf->gen_packed;
+    a.lambs_e = cf->lambs_e; a.mus_e = cf->mus_e;
+    if ((a.lambs_e == nullptr) != (a.mus_e == nullptr))
+        return set_error(SA_ERR_ARG, "per-element lambs_e and mus_e must be given together");
     memcpy(a.A_const, cf->A_const, sizeof a.A_const);
     a.a0_const = cf->a0_const;
     const double den = (double)((d + 1) * (d + 2) * (d + 3));
@@ -2997,6 +2212,8 @@ int sa_numeric(sa_plan *P, int ops, const sa_coeffs *cf, double *const *vals_dev
         a.ne = P->e_hi - P->e_lo;
         a.tp_rank = P->tp_rank;
         a.wseg = P->wseg;
+        a.nflag = P->gd_nflag;
+        a.flag_rows = P->gd_flag_rows;
     }
     SA_CUDA_TRY(cudaMemsetAsync(P->counters, 0, 4 * sizeof(int64_t), st));
     SA_CUDA_TRY(cudaMemsetAsync(P->counters + 4, 0x7f, sizeof(int64_t), st));

@@ -42,6 +42,12 @@ __device__ __forceinline__ void ldg256(const void *p, double &a, double &b, doub
     asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
 }
 
+// streaming (evict-first) 32-byte load: data read exactly once
+__device__ __forceinline__ void ldg256_cs(const void *p, double &a, double &b, double &c, double &d)
+{
+    asm("ld.global.cs.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+
 template <int D>
 __device__ __forceinline__ void load_vertex(const typename VecT<D>::type *__restrict__ qv, int v, double (&x)[D])
 {

@@ -1,6 +1,8 @@
 // sa_scan.cu -- device-wide exclusive scan (int64) and error plumbing.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "sa_common.cuh"
 
@@ -10,6 +12,37 @@ ErrState &err_state()
 {
     static thread_local ErrState s;
     return s;
+}
+
+static const char *tune_find(const char *key, size_t *len)
+{
+    const char *t = getenv("SA_TUNE");
+    if (!t) return nullptr;
+    const size_t kl = strlen(key);
+    for (const char *p = t; *p;) {
+        const char *e = strchr(p, ',');
+        const size_t n = e ? (size_t)(e - p) : strlen(p);
+        if (n > kl && strncmp(p, key, kl) == 0 && p[kl] == '=') {
+            *len = n - kl - 1;
+            return p + kl + 1;
+        }
+        p += n + (e ? 1 : 0);
+    }
+    return nullptr;
+}
+
+int tune_int(const char *key, int dflt)
+{
+    size_t n = 0;
+    const char *v = tune_find(key, &n);
+    return v && n ? atoi(v) : dflt;
+}
+
+bool tune_is(const char *key, const char *value)
+{
+    size_t n = 0;
+    const char *v = tune_find(key, &n);
+    return v && n == strlen(value) && strncmp(v, value, n) == 0;
 }
 
 int set_error(int status, const char *fmt, ...)

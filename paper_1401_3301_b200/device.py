@@ -157,10 +157,10 @@ class Plan:
         return self._h
 
     def stats(self) -> dict:
-        out = (ctypes.c_int64 * 12)()
-        _lib.check(_lib.load().sa_plan_stats(self._h, out, 12))
-        keys = ("templates", "templates_ok", "fold_ok", "incidences", "template_words", "max_row_nodes",
-                "nodes", "nnz", "chunk_ok", "chunks", "chunk_templates", "chunk_template_words")
+        out = (ctypes.c_int64 * 8)()
+        _lib.check(_lib.load().sa_plan_stats(self._h, out, 8))
+        keys = ("incidences", "max_row_nodes", "nodes", "nnz", "warp_records", "twopass_slots",
+                "element_batches_staged", "max_batch_vertices")
         return dict(zip(keys, [int(x) for x in out]))
 
     def pattern(self, stream=None):
@@ -191,6 +191,9 @@ class Plan:
                     c.w = up(k.w)
                 else:
                     c.w_const = k.w_const
+            elif k.op == "elastic" and getattr(k, "lambs_e", None) is not None:
+                c.lambs_e = up(k.lambs_e)
+                c.mus_e = up(k.mus_e)
             elif k.op == "elastic":
                 if k.lamb is not None:
                     c.lamb = up(k.lamb)
@@ -245,6 +248,8 @@ class Plan:
         ops = 0
         for k in kernels:
             ops |= OP_BITS[k.op]
+            if getattr(k, "exact", False):
+                ops |= _lib.SA_OP_EXACT
         order = sorted(kernels, key=lambda k: OP_BITS[k.op])
         n = len(order)
         dev = self.dmesh.device

@@ -75,6 +75,28 @@ class ElasticKernel:
         if np.any(bad):
             node = int(np.flatnonzero(bad)[0])
             raise ValueError(f"Lame parameters must satisfy lamb + mu > 0; violated at node {node}")
+        self.lambs_e = self.mus_e = None
+
+    @classmethod
+    def per_element(cls, mesh, lambs, mus):
+        """Descriptor from per-element Lame sums already scaled by
+        vols/(d+1) -- exactly the ``lambs``/``mus`` arrays the reference's
+        ElasticKernel keeps (kernels.py:354-356); the device uses them as
+        given, so the values are bitwise the reference's."""
+        self = cls.__new__(cls)
+        d = mesh.q.shape[0]
+        if d not in (2, 3):
+            raise ValueError(f"elastic tables are defined for d in {{2, 3}}, got {d}")
+        nme = mesh.me.shape[1]
+        self.mesh = mesh
+        self.d = self.m = d
+        self.lamb = self.mu = None
+        self.lamb_const = self.mu_const = 1.0
+        self.lambs_e = np.ascontiguousarray(np.asarray(lambs, dtype=np.float64))
+        self.mus_e = np.ascontiguousarray(np.asarray(mus, dtype=np.float64))
+        if self.lambs_e.shape != (nme,) or self.mus_e.shape != (nme,):
+            raise ValueError(f"lambs/mus must have shape ({nme},), got {self.lambs_e.shape} and {self.mus_e.shape}")
+        return self
 
 
 def _field(value, q, shape_tail, name):
@@ -100,7 +122,8 @@ def _field(value, q, shape_tail, name):
 class GeneralKernel:
     """General second-order operator -div(A grad u) + div(b u) + c.grad u + a0 u
     (weak form and quadrature in DESIGN.md 3.4).  Row = test
-    function, as in the reference.  Not symmetric in general.
+    function, as in the reference.  Not symmetric in general.  ``exact``
+    selects bitwise reference-order element arithmetic (see below).
 
     A: (d, d) constant, (nq, d, d) nodal array or callable q -> (d, d, nq);
     b, c: (d,) constant, (nq, d) nodal or callable q -> (d, nq); a0: scalar,
@@ -109,7 +132,7 @@ class GeneralKernel:
     op = "general"
     m = 1
 
-    def __init__(self, mesh, A=None, b=None, c=None, a0=None):
+    def __init__(self, mesh, A=None, b=None, c=None, a0=None, exact=False):
         q = mesh.q
         d = q.shape[0]
         if d not in (1, 2, 3):
@@ -127,6 +150,12 @@ class GeneralKernel:
         else:
             self.a0, self.a0_const = nodal_values(a0, q)
         self.symmetric = False
+        # exact=True: element values in the reference's operation order
+        # (bitwise the oracle).  Default: fused multiply-adds in the local
+        # matrix (values within a few ulp of the contributions, far inside the
+        # 1e-12-of-row-max bar); the exact-zero pattern is the reference's in
+        # both modes (guarded rows are recomputed in reference order).
+        self.exact = bool(exact)
         self._packed = None
 
     def packed(self) -> np.ndarray:

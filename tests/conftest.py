@@ -66,7 +66,7 @@ def device_kernel_for(name, g, mesh):
     if kind == "elasticc":
         return P.ElasticKernel(mesh, 1.0, 0.5)
     if kind == "general":
-        return P.GeneralKernel(mesh, A=g["A"], b=g["b"], c=g["c"], a0=g["a0"])
+        return P.GeneralKernel(mesh, A=g["A"], b=g["b"], c=g["c"], a0=g["a0"], exact=True)
     raise KeyError(name)
 
 

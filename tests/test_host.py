@@ -122,6 +122,41 @@ def test_register_into_reference_registries():
         sys.path.remove(ref)
 
 
+def test_reference_problem_elastic_reaches_device_call():
+    # the reference's own bench dispatch, VECTOR_DRIVERS["b200"](ctx,
+    # ElasticKernel(ctx)) (bench.py:146-153): the reference kernel object is
+    # accepted (its per-element lambs/mus become the descriptor) and the call
+    # gets as far as the device -- on a CPU-only host that is the loud
+    # ExtensionMissingError, never a TypeError
+    import importlib
+    import sys
+
+    ref = "/root/reference/pkg/src"
+    if not os.path.isdir(ref):
+        pytest.skip("reference tree not present (GPU box)")
+    sys.path.insert(0, ref)
+    try:
+        rb = importlib.import_module("simplex_asm.bench")
+        from paper_1401_3301_b200 import assembly, kernels
+        from paper_1401_3301_b200.errors import ExtensionMissingError
+
+        assert assembly.register()
+        prob = rb._Problem("elastic", 2)
+        ctx = prob.setup(4)
+        rk = importlib.import_module("simplex_asm.kernels").ElasticKernel(ctx, 1.0, 0.5)
+        desc = assembly._as_descriptor(ctx, rk)
+        assert isinstance(desc, kernels.ElasticKernel) and desc.m == 2
+        assert np.array_equal(desc.lambs_e, rk.lambs) and np.array_equal(desc.mus_e, rk.mus)
+        import torch
+
+        if torch.cuda.is_available():
+            pytest.skip("CPU-only check")
+        with pytest.raises(ExtensionMissingError):
+            prob.assemble(ctx, "b200")
+    finally:
+        sys.path.remove(ref)
+
+
 def test_slabs_reproduce_full_rows_bitwise():
     # P row blocks assembled from their slabs (elements touching the block,
     # local node window) stitch to the full optv2 matrix, bitwise

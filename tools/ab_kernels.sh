@@ -5,7 +5,7 @@ cd "${GRAFT_REPO_ROOT:-$(dirname $0)/..}"
 mkdir -p gpurun_out
 for CFG in ${CFGS:-C2 C3 C4 C5}; do
   for K in ${KERNELS:-rowgather twopass}; do
-    SA_KERNEL=$K timeout 900 python bench.py --config $CFG --steps ${STEPS:-10} --warmup 3 --no-e2e --no-cpu-baseline \
+    SA_TUNE=kernel=$K timeout 900 python bench.py --config $CFG --steps ${STEPS:-10} --warmup 3 --no-e2e --no-cpu-baseline \
       > gpurun_out/ab_${CFG}_${K}.log 2>&1
     python - "$CFG" "$K" <<'PY'
 import json, sys
