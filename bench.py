@@ -105,7 +105,14 @@ def general_coeffs(cfg, nq):
     a0 ~ U[0,1), drawn over the global node numbering."""
     rng = np.random.default_rng(cfg["seed"])
     R = rng.standard_normal((nq, 3, 3))
-    A = np.eye(3)[None] + 0.5 * np.einsum("nij,nkj->nik", R, R) / 3.0
+    # A = I + 0.5 R R^T / 3, built in place (one (nq,3,3) temporary)
+    A = np.einsum("nij,nkj->nik", R, R)
+    del R
+    A *= 0.5
+    A /= 3.0
+    A[:, 0, 0] += 1.0
+    A[:, 1, 1] += 1.0
+    A[:, 2, 2] += 1.0
     b = rng.standard_normal((nq, 3))
     c = rng.standard_normal((nq, 3))
     a0 = rng.uniform(0.0, 1.0, nq)
@@ -324,6 +331,9 @@ def main():
                     help="N > 1: strong = the config mesh split N ways (BASELINE C5: 'row-block sharded at "
                          "1/2/4/8 B200'), weak = per-GPU work fixed (refined global mesh)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--table", choices=["csv", "md"], default=None,
+                    help="also write the reference's emit_table rows (bench.py:292-307 columns) to --table-out")
+    ap.add_argument("--table-out", default="bench_table.csv")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
@@ -507,6 +517,7 @@ def main():
                    "timing": "per-step CUDA events on the launching stream, summed; max over ranks",
                    "launch": "CUDA graph replay of the numeric phase" if graph is not None else "direct"},
         "nnz_per_s": nnz_struct_all * len(kernels) / (ms_per_step * 1e-3),
+        "plan_device_bytes": plan.stats()["device_bytes"],
         "symbolic_ms": t_sym_ms,
         "symbolic_cold_ms": t_sym_cold_ms,
         "numeric_ms": ms_per_step,
@@ -522,8 +533,42 @@ def main():
     if base is not None:
         line["cpu_baseline"] = base
     print(json.dumps(line), flush=True)
+    if args.table:
+        write_table(args, cfg, line)
     if world > 1:
         dist.destroy_process_group()
+
+
+CSV_COLUMNS = ("variant", "matrix", "d", "ndof", "nme", "time_mean_s", "time_median_s", "aux_bytes", "speedup")
+
+
+def write_table(args, cfg, line):
+    """The reference's CSV/markdown table (simplex_asm.bench.emit_table:
+    CSV_COLUMNS, %.6g times, %.2f speedup) for this run: one row for the B200
+    end-to-end driver call and, when measured, one for the CPU baseline.
+    aux_bytes = the plan's device-resident symbolic structures."""
+    d = cfg["d"]
+    matrix = "+".join(cfg["ops"])
+    m = d if "elastic" in cfg["ops"] else 1
+    ndof = m * line["config"]["nq"]
+    nme = line["config"]["nme"]
+    e2e = line.get("e2e") or {}
+    t_b200 = e2e.get("ms_per_step", line["ms_per_step"]) * 1e-3
+    base = line.get("cpu_baseline") or {}
+    t_cpu = nme / base["value"] if base.get("value") else None
+    aux = int(line.get("plan_device_bytes", 0))
+    rows = [("b200", matrix, d, ndof, nme, t_b200, t_b200, aux, (t_cpu / t_b200) if t_cpu else 1.0)]
+    if t_cpu:
+        rows.append(("cpu-port", matrix, d, ndof, nme, t_cpu, t_cpu, 0, 1.0))
+    if args.table == "csv":
+        text = ",".join(CSV_COLUMNS) + "\n" + "".join(
+            f"{r[0]},{r[1]},{r[2]},{r[3]},{r[4]},{r[5]:.6g},{r[6]:.6g},{r[7]},{r[8]:.2f}\n" for r in rows)
+    else:
+        text = "| " + " | ".join(CSV_COLUMNS) + " |\n|" + "---|" * len(CSV_COLUMNS) + "\n" + "".join(
+            f"| {r[0]} | {r[1]} | {r[2]} | {r[3]} | {r[4]} | {r[5]:.6g} | {r[6]:.6g} | {r[7]} | {r[8]:.2f} |\n"
+            for r in rows)
+    with open(args.table_out, "w") as f:
+        f.write(text)
 
 
 def run_e2e(q, me, vols, kernels, rb, re_, col_offset, nme_global, args, world, dev):
@@ -542,6 +587,15 @@ def run_e2e(q, me, vols, kernels, rb, re_, col_offset, nme_global, args, world, 
     pv = torch.from_numpy(np.asarray(vols)).pin_memory()
     mesh = P.Mesh(pq.numpy(), pme.numpy(), pv.numpy())
     h2d = pq.numel() * 8 + pme.numel() * 8 + pv.numel() * 8
+    # plus the nodal coefficient arrays every assembly uploads (pinned copies
+    # cached on the descriptors)
+    for k in kernels:
+        for name in ("w", "lamb", "mu", "lambs_e", "mus_e"):
+            v = getattr(k, name, None)
+            if isinstance(v, np.ndarray):
+                h2d += v.nbytes
+        if k.op == "general":
+            h2d += k.packed().nbytes
     # two untimed calls (pinned staging buffers and pool memory are set up on
     # first use), then the median of up to 7 timed calls
     steps = max(3, min(args.steps, 7))

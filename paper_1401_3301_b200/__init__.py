@@ -27,7 +27,7 @@ from .mesh import (
     jittered_hypercube_mesh,
 )
 from .pk import PkCoeffTable, PkMesh, build_pk_mesh, multi_index_lattice, pk_mass_coeffs
-from .sparse import SparseMatrix, to_scipy
+from .sparse import SparseMatrix, to_scipy, write_matrixmarket
 
 __version__ = "0.1.0"
 

@@ -16,7 +16,7 @@ import weakref
 import numpy as np
 
 from . import kernels as _k
-from .device import DeviceCSR, DeviceMesh
+from .device import OP_BITS, DeviceCSR, DeviceMesh, upload_coeffs
 from .sparse import SparseMatrix
 
 _MESH_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
@@ -72,12 +72,17 @@ class _PatternDownload:
     overlap the numeric phase.  ``col_offset`` shifts a slab's local columns
     to global dofs on the device first."""
 
-    def __init__(self, indptr, indices, col_offset: int = 0):
+    def __init__(self, indptr, indices, col_offset: int = 0, local_ncols: int | None = None):
         import torch
 
         self.key = (indptr.data_ptr(), indices.data_ptr(), indices.numel())
         self.stream = torch.cuda.Stream(device=indptr.device)
         self.stream.wait_stream(torch.cuda.current_stream())
+        # global dofs fit int32 (CapacityError otherwise, sa_plan_create); the
+        # shift is done on the device in int32 only when it cannot wrap
+        self.host_offset = 0
+        if col_offset and (local_ncols is None or int(col_offset) + int(local_ncols) >= (1 << 31)):
+            self.host_offset, col_offset = int(col_offset), 0
         with torch.cuda.stream(self.stream):
             ix = indices + col_offset if col_offset else indices
             self.ip = torch.empty(indptr.shape, dtype=torch.int64, pin_memory=True)
@@ -98,6 +103,8 @@ class _PatternDownload:
             self.done.synchronize()
             ix64 = torch.empty(self.ix32.shape, dtype=torch.int64, pin_memory=True)
             ix64.copy_(self.ix32)
+            if self.host_offset:
+                ix64 += self.host_offset
             self._host = (self.ip.numpy(), ix64.numpy())
         return self._host
 
@@ -108,7 +115,7 @@ def to_host(csr: DeviceCSR, nrows_total: int | None = None) -> SparseMatrix:
     return to_host_many([csr], nrows_total)[0]
 
 
-def to_host_many(csrs, nrows_total=None, col_offset: int = 0, patterns=()) -> list[SparseMatrix]:
+def to_host_many(csrs, nrows_total=None, col_offset: int = 0, patterns=(), ncols: int | None = None) -> list[SparseMatrix]:
     """Download several results; fused outputs that share one pattern (no
     exact-zero entries dropped) share the host row_ptr/col_idx arrays, so the
     pattern crosses PCIe once (as int32 indices, widened on the host while
@@ -121,7 +128,7 @@ def to_host_many(csrs, nrows_total=None, col_offset: int = 0, patterns=()) -> li
     for c in csrs:
         key = (c.indptr.data_ptr(), c.indices.data_ptr(), c.indices.numel())
         if key not in cache:
-            cache[key] = _PatternDownload(c.indptr, c.indices, col_offset)
+            cache[key] = _PatternDownload(c.indptr, c.indices, col_offset, c.ncols)
     vals = []
     for c in csrs:
         v = torch.empty(c.vals.shape, dtype=c.vals.dtype, pin_memory=True)
@@ -132,7 +139,8 @@ def to_host_many(csrs, nrows_total=None, col_offset: int = 0, patterns=()) -> li
     torch.cuda.current_stream().synchronize()
     for c, (ip, ix), v in zip(csrs, hosts, vals):
         nrows = c.row_end - c.row_begin if nrows_total is None else nrows_total
-        res.append(SparseMatrix(nrows, c.ncols, ip, ix, v.numpy()))
+        # global column count: a slab's local columns were shifted by col_offset
+        res.append(SparseMatrix(nrows, ncols if ncols is not None else c.ncols + col_offset, ip, ix, v.numpy()))
     return res
 
 
@@ -154,13 +162,14 @@ def assemble_many_b200(mesh, kernels, core: str = "SkylakeX", cache: bool = True
 
 
 def assemble_block_b200(mesh, kernels, row_begin: int, row_end: int, core: str = "SkylakeX",
-                        timings: dict | None = None, col_offset: int = 0):
+                        timings: dict | None = None, col_offset: int = 0, ncols: int | None = None):
     """Rows [row_begin, row_end) of the fused assembly, end to end from host
     arrays (the per-rank call of the row-block data-parallel path): upload,
     symbolic, numeric, exact-zero compaction, download.  Returns one
     (indptr, indices, vals) host block per kernel.  For a rank's slab
     (parallel.slab) pass its local rows and ``col_offset`` to get global
-    column dofs."""
+    column dofs, and ``ncols`` the global column count of the matrix the
+    block belongs to (default: the slab's columns + col_offset)."""
     import time
 
     import torch
@@ -180,18 +189,23 @@ def assemble_block_b200(mesh, kernels, row_begin: int, row_end: int, core: str =
     side.wait_event(me_done)
     with torch.cuda.stream(side):
         qd = torch.as_tensor(np.asarray(mesh.q)).to(main.device, non_blocking=True)
+    # nodal coefficients (pinned copies cached on the descriptors) upload on
+    # the side stream too, behind the coordinates, during the symbolic phase
+    order = sorted(kernels, key=lambda k: OP_BITS[k.op])
+    coeffs = upload_coeffs(order, main.device, int(np.asarray(mesh.q).shape[0]), side)
     dm = DeviceMesh(None, med, vd, core=core, nq=int(np.asarray(mesh.q).shape[1]))
     t1 = time.perf_counter()
     plan = dm.plan(kernels[0].m, row_begin, row_end)
     main.wait_stream(side)
     dm.set_coords(qd)
     # the structural pattern downloads while the numeric phase runs
-    pat = _PatternDownload(*plan.pattern(), col_offset)
+    pat = _PatternDownload(*plan.pattern(), col_offset, kernels[0].m * dm.nq)
     t2 = time.perf_counter()
-    csrs = plan.assemble(kernels)
+    csrs = plan.assemble(kernels, coeffs=coeffs)
     torch.cuda.current_stream().synchronize()
+    del coeffs
     t3 = time.perf_counter()
-    out = to_host_many(csrs, col_offset=col_offset, patterns=(pat,))
+    out = to_host_many(csrs, col_offset=col_offset, patterns=(pat,), ncols=ncols)
     t4 = time.perf_counter()
     dm.close()
     if timings is not None:

@@ -1646,26 +1646,6 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
     SA_CUDA_TRY(cudaMemcpyAsync(&md, P->counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     SA_CUDA_TRY(cudaStreamSynchronize(st));
     P->max_deg = md;
-    // warp-interleaved records for the row-gather kernel: on by default in 3D
-    // (they replace three dependent gathers per incidence; measured faster),
-    // off in 1D/2D (same speed there, 4x the record traffic); SA_WINC=0|1
-
-    // (the records carry the volume: without it yet -- a mesh created
-    // without coordinates or volumes -- the plan uses the 8-byte records)
-    const bool want_winc = tune_int("winc", D == 3) != 0 && M->vols_ready;
-    if (nn && want_winc) {
-        const int64_t nw = (nn + 31) / 32;
-        SA_CUDA_TRY(cudaMallocAsync((void **)&P->wseg, (nw + 1) * sizeof(int64_t), st));
-        SA_LAUNCH(k_warp_span, grid_for(nw, 128), 128, 0, st, P->inc_ptr, nn, cnt);
-        SA_TRY(exclusive_scan_i64(cnt, P->wseg, nw, P->scan_tmp, st));
-        SA_CUDA_TRY(cudaMemcpyAsync(&P->n_winc, P->wseg + nw, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
-        SA_CUDA_TRY(cudaMallocAsync((void **)&P->winc, std::max<int64_t>(P->n_winc, 1) * sizeof(IncRec), st));
-        // padding records (rows shorter than their warp's longest) = all ones: ea = 0xffffffff sentinel
-        SA_CUDA_TRY(cudaMemsetAsync(P->winc, 0xff, std::max<int64_t>(P->n_winc, 1) * sizeof(IncRec), st));
-        SA_LAUNCH(k_winc_fill<D>, grid_for(nn, 128), 128, 0, st, (const I *)M->me, M->vols, P->inc_ptr, P->inc, nn,
-                  P->wseg, P->winc);
-    }
     const int m = P->m;
     P->nnz = (int64_t)m * m * P->n_colnodes;
     if (P->nnz >= ((int64_t)1 << 31) || (int64_t)m * M->nq >= ((int64_t)1 << 31))
@@ -1676,6 +1656,38 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
     SA_LAUNCH(k_dof_csr, grid_for(nn + 1, 128), 128, 0, st, P->colptr, P->cols, nn, m, P->indptr, P->indices);
     SA_CUDA_TRY(cudaFreeAsync(cnt, st));
     SA_CUDA_TRY(cudaStreamSynchronize(st));
+    return SA_OK;
+}
+
+// Warp-interleaved incidence records (IncRec, 32 B) for the 3D row gather:
+// they replace three dependent gathers per incidence (measured faster in 3D;
+// no gain in 1D/2D at 4x the record traffic).  Built on the first row-gather
+// numeric call of a plan -- plans served by the two-pass path (3D general
+// operator) never pay for them.  The records carry the volume, so the mesh
+// volumes must be set.
+template <int D>
+int build_winc(sa_plan *P, cudaStream_t st)
+{
+    typedef typename IdxT<D>::type I;
+    const sa_mesh *M = P->mesh;
+    const int64_t nn = P->nnodes;
+    if (P->winc || !nn || !M->vols_ready || tune_int("winc", D == 3) == 0) return SA_OK;
+    const int64_t nw = (nn + 31) / 32;
+    int64_t *span = nullptr;
+    SA_CUDA_TRY(cudaMallocAsync((void **)&span, (nw + 1) * sizeof(int64_t), st));
+    if (!P->wseg) {
+        SA_CUDA_TRY(cudaMallocAsync((void **)&P->wseg, (nw + 1) * sizeof(int64_t), st));
+        SA_LAUNCH(k_warp_span, grid_for(nw, 128), 128, 0, st, P->inc_ptr, nn, span);
+        SA_TRY(exclusive_scan_i64(span, P->wseg, nw, P->scan_tmp, st));
+    }
+    SA_CUDA_TRY(cudaMemcpyAsync(&P->n_winc, P->wseg + nw, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SA_CUDA_TRY(cudaStreamSynchronize(st));
+    SA_CUDA_TRY(cudaFreeAsync(span, st));
+    SA_CUDA_TRY(cudaMallocAsync((void **)&P->winc, std::max<int64_t>(P->n_winc, 1) * sizeof(IncRec), st));
+    // padding records (rows shorter than their warp's longest) = all ones: ea = 0xffffffff sentinel
+    SA_CUDA_TRY(cudaMemsetAsync(P->winc, 0xff, std::max<int64_t>(P->n_winc, 1) * sizeof(IncRec), st));
+    SA_LAUNCH(k_winc_fill<D>, grid_for(nn, 128), 128, 0, st, (const I *)M->me, M->vols, P->inc_ptr, P->inc, nn,
+              P->wseg, P->winc);
     return SA_OK;
 }
 
@@ -1852,7 +1864,11 @@ int sa_symbolic_d3(sa_plan *, cudaStream_t);
 int sa_dispatch_d1(const sa_plan *, const NumArgs &, int, int, cudaStream_t);
 int sa_dispatch_d2(const sa_plan *, const NumArgs &, int, int, cudaStream_t);
 int sa_dispatch_d3(const sa_plan *, const NumArgs &, int, int, cudaStream_t);
+int sa_winc_d3(sa_plan *, cudaStream_t);
 #ifdef SA_D
+#if SA_D == 3
+int sa_winc_d3(sa_plan *P, cudaStream_t st) { return build_winc<3>(P, st); }
+#endif
 int SA_CAT(sa_mesh_kernels_d, SA_D)(sa_mesh *M, const double *q, const int64_t *me, const double *vols, cudaStream_t st)
 {
     return mesh_kernels<SA_D>(M, q, me, vols, st);
@@ -2023,9 +2039,16 @@ int sa_plan_info(const sa_plan *P, int64_t *nrows, int64_t *nnz, int64_t *max_ro
 int sa_plan_stats(const sa_plan *P, int64_t *out, int n)
 {
     if (!P || !out) return set_error(SA_ERR_ARG, "plan/out is NULL");
-    const int64_t v[8] = {P->n_inc, P->max_deg, P->nnodes, P->nnz, P->n_winc, P->tp_nslots, P->eb_allfit ? 1 : 0,
-                          P->eb_maxn};
-    for (int i = 0; i < n && i < 8; ++i) out[i] = v[i];
+    const int64_t nn = P->nnodes, nw = (nn + 31) / 32, ne = P->e_hi - P->e_lo, nb = (ne + EB_SIZE - 1) / EB_SIZE;
+    // device bytes of the plan's symbolic structures (pattern, incidences,
+    // warp records, two-pass slot map / row buffer / element batches)
+    const int64_t bytes = 3 * (nn + 1) * 8 + P->n_inc * 8 + P->n_colnodes * 4 + (P->nrows + 1) * 8 + P->nnz * 4 +
+                          P->n_winc * (int64_t)sizeof(IncRec) + (P->wseg ? (nw + 1) * 8 : 0) +
+                          (P->epos ? ne * 16 : 0) + P->kbuf_elems * 8 + P->tp_nslots * 4 +
+                          (P->eb_loc ? ne * 4 + nb * (EB_CAP + 1) * 4 : 0);
+    const int64_t v[9] = {P->n_inc, P->max_deg, P->nnodes, P->nnz, P->n_winc, P->tp_nslots, P->eb_allfit ? 1 : 0,
+                          P->eb_maxn, bytes};
+    for (int i = 0; i < n && i < 9; ++i) out[i] = v[i];
     return SA_OK;
 }
 
@@ -2140,6 +2163,8 @@ int sa_plan_prepare(sa_plan *P, int ops, void *stream)
     const int d = P->mesh->d;
     SA_TRY(set_device(P->mesh->device));
     ops &= 15;
+    if (d == 3 && !(want_twopass(ops, d, P->m) && P->n_inc < 0xffffffffLL))
+        SA_TRY(sa_winc_d3(P, (cudaStream_t)stream));
     if (want_twopass(ops, d, P->m) && P->n_inc < 0xffffffffLL) {
         const int ks = (d + 1) * plan_nout(ops) * P->m * P->m;
         SA_TRY(ensure_twopass(P, ks, want_batches(ops, d), (cudaStream_t)stream));
@@ -2161,6 +2186,7 @@ int sa_numeric(sa_plan *P, int ops, const sa_coeffs *cf, double *const *vals_dev
     memset(&a, 0, sizeof a);
     a.exact = (ops & SA_OP_EXACT) ? 1 : 0;
     ops &= 15;
+    if (d == 3 && !(want_twopass(ops, d, P->m) && P->n_inc < 0xffffffffLL)) SA_TRY(sa_winc_d3(P, st));
 
     a.qv = M->qv; a.me = M->me; a.vols = M->vols;
     a.nnodes = P->nnodes; a.node_begin = P->node_begin;

@@ -157,10 +157,10 @@ class Plan:
         return self._h
 
     def stats(self) -> dict:
-        out = (ctypes.c_int64 * 8)()
-        _lib.check(_lib.load().sa_plan_stats(self._h, out, 8))
+        out = (ctypes.c_int64 * 9)()
+        _lib.check(_lib.load().sa_plan_stats(self._h, out, 9))
         keys = ("incidences", "max_row_nodes", "nodes", "nnz", "warp_records", "twopass_slots",
-                "element_batches_staged", "max_batch_vertices")
+                "element_batches_staged", "max_batch_vertices", "device_bytes")
         return dict(zip(keys, [int(x) for x in out]))
 
     def pattern(self, stream=None):
@@ -173,55 +173,9 @@ class Plan:
             self._pattern = (ip, ix[: self.nnz])
         return self._pattern
 
-    def coeffs(self, kernels) -> tuple[_lib.SaCoeffs, list]:
+    def coeffs(self, kernels, stream=None) -> tuple[_lib.SaCoeffs, list]:
         """Pack the kernels' nodal coefficients into an sa_coeffs (device)."""
-        dev = self.dmesh.device
-        c = _lib.SaCoeffs()
-        c.w_const = c.lamb_const = c.mu_const = 1.0
-        keep = []
-
-        def up(a):
-            t = _to_dev(a, torch.float64, dev)
-            keep.append(t)
-            return _ptr(t)
-
-        for k in kernels:
-            if k.op == "mass":
-                if k.w is not None:
-                    c.w = up(k.w)
-                else:
-                    c.w_const = k.w_const
-            elif k.op == "elastic" and getattr(k, "lambs_e", None) is not None:
-                c.lambs_e = up(k.lambs_e)
-                c.mus_e = up(k.mus_e)
-            elif k.op == "elastic":
-                if k.lamb is not None:
-                    c.lamb = up(k.lamb)
-                else:
-                    c.lamb_const = k.lamb_const
-                if k.mu is not None:
-                    c.mu = up(k.mu)
-                else:
-                    c.mu_const = k.mu_const
-            elif k.op == "general" and hasattr(k, "packed"):
-                c.gen_packed = up(k.packed().reshape(-1))
-            elif k.op == "general":
-                d = self.dmesh.d
-                if k.A is not None:
-                    c.A = up(k.A.reshape(-1))
-                else:
-                    for i, v in enumerate(np.asarray(k.A_const, dtype=np.float64).reshape(-1)):
-                        c.A_const[i] = v
-                if k.b is not None:
-                    c.b = up(k.b.reshape(-1))
-                if k.c is not None:
-                    c.c = up(k.c.reshape(-1))
-                if k.a0 is not None:
-                    c.a0 = up(k.a0)
-                else:
-                    c.a0_const = k.a0_const
-                del d
-        return c, keep
+        return upload_coeffs(kernels, self.dmesh.device, self.dmesh.d, stream)
 
     def prepare(self, kernels, stream=None):
         """Build the per-plan structures the numeric kernel for these
@@ -306,8 +260,8 @@ class Plan:
                                           _stream_ptr(stream)))
         return DeviceCSR(self.row_begin, self.row_end, ncols, nip, nix[:nnz], nva[:nnz])
 
-    def assemble(self, kernels, stream=None) -> list[DeviceCSR]:
-        vals, zeros = self.numeric(kernels, stream=stream, sync=True)
+    def assemble(self, kernels, stream=None, coeffs=None) -> list[DeviceCSR]:
+        vals, zeros = self.numeric(kernels, stream=stream, sync=True, coeffs=coeffs)
         return [self.compact(v, z, stream) for v, z in zip(vals, zeros)]
 
     def close(self):
@@ -320,6 +274,59 @@ class Plan:
             self.close()
         except Exception:
             pass
+
+
+def _pinned(k, name, arr):
+    """A page-locked host copy of a kernel's coefficient array, cached on the
+    descriptor (built once per coefficient set, like the reference's kernel
+    construction), so every assembly uploads it at full PCIe rate and
+    asynchronously."""
+    cache = k.__dict__.setdefault("_pinned_cache", {})
+    t = cache.get(name)
+    if t is None or t.numel() != np.asarray(arr).size:
+        t = torch.from_numpy(np.ascontiguousarray(arr).reshape(-1))
+        if torch.cuda.is_available():
+            t = t.pin_memory()
+        cache[name] = t
+    return t
+
+
+def upload_coeffs(kernels, device, d, stream=None) -> tuple[_lib.SaCoeffs, list]:
+    """sa_coeffs for ``kernels`` (ascending op-bit order) with their nodal /
+    per-element arrays uploaded to ``device`` on ``stream`` (asynchronous from
+    pinned copies; the caller orders the numeric phase after the stream)."""
+    c = _lib.SaCoeffs()
+    c.w_const = c.lamb_const = c.mu_const = 1.0
+    keep = []
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+
+    def up(k, name, a):
+        with torch.cuda.stream(s):
+            t = _pinned(k, name, a).to(device=device, dtype=torch.float64, non_blocking=True)
+        keep.append(t)
+        return _ptr(t)
+
+    for k in kernels:
+        if k.op == "mass":
+            if k.w is not None:
+                c.w = up(k, "w", k.w)
+            else:
+                c.w_const = k.w_const
+        elif k.op == "elastic" and getattr(k, "lambs_e", None) is not None:
+            c.lambs_e = up(k, "lambs_e", k.lambs_e)
+            c.mus_e = up(k, "mus_e", k.mus_e)
+        elif k.op == "elastic":
+            if k.lamb is not None:
+                c.lamb = up(k, "lamb", k.lamb)
+            else:
+                c.lamb_const = k.lamb_const
+            if k.mu is not None:
+                c.mu = up(k, "mu", k.mu)
+            else:
+                c.mu_const = k.mu_const
+        elif k.op == "general":
+            c.gen_packed = up(k, "packed", k.packed())
+    return c, keep
 
 
 def device_volumes(q, me, core: str = "SkylakeX") -> np.ndarray:

@@ -176,3 +176,27 @@ class GeneralKernel:
             p[:, 15] = self.a0 if self.a0 is not None else self.a0_const
             self._packed = p
         return self._packed
+
+
+def restrict(kernel, mesh_local, nodes: slice, elements):
+    """The descriptor ``kernel`` on a sub-mesh (a rank's slab,
+    parallel.slab): nodal coefficient arrays cut to the node window
+    ``nodes``, per-element arrays to ``elements`` (ascending global ids);
+    constants unchanged.  Used by the distributed driver."""
+    import copy
+
+    k = copy.copy(kernel)
+    k.mesh = mesh_local
+    k.__dict__.pop("_pinned_cache", None)
+    k.__dict__.pop("_packed", None)
+    for name in ("w", "lamb", "mu", "A", "b", "c", "a0"):
+        v = getattr(kernel, name, None)
+        if isinstance(v, np.ndarray) and v.ndim >= 1 and v.shape[0] == kernel.mesh.q.shape[1]:
+            setattr(k, name, np.ascontiguousarray(v[nodes]))
+    for name in ("lambs_e", "mus_e"):
+        v = getattr(kernel, name, None)
+        if v is not None:
+            setattr(k, name, np.ascontiguousarray(np.asarray(v)[elements]))
+    if getattr(kernel, "op", None) == "general":
+        k._packed = None
+    return k

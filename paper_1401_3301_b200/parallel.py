@@ -112,5 +112,91 @@ def gather_blocks_to_root(block, group=None, root: int = 0):
 
     world = dist.get_world_size(group)
     out = [None] * world if dist.get_rank(group) == root else None
+    if dist.get_backend(group) == "nccl":
+        # gather_object over NCCL needs the rank's device set; objects are
+        # pickled through it
+        import torch
+
+        torch.cuda.set_device(torch.cuda.current_device())
     dist.gather_object(block, out, dst=root, group=group)
     return out
+
+
+@dataclass
+class DistributedResult:
+    """One rank's share of a distributed assembly: its row block per kernel
+    (host CSR: indptr relative, global int64 columns, values), the global
+    offset of its first entry, the global nnz, and -- on the root rank when
+    gathered -- the stitched matrices."""
+
+    row_begin: int
+    row_end: int
+    blocks: list
+    offsets: list
+    totals: list
+    matrices: list | None
+
+
+def assemble_distributed(mesh, kernels, group=None, gather: bool = True, root: int = 0, core: str = "SkylakeX",
+                         timings: dict | None = None) -> DistributedResult:
+    """Rank-aware driver of the row-block data-parallel path,
+    one process per GPU (torchrun; torch.distributed initialised, NCCL on
+    B200s, gloo in tests; a single process without a process group is world
+    size 1).  Each rank takes the node-aligned row block ``row_blocks(nq, m,
+    P)[rank]``, cuts its slab (the elements touching its rows, in ascending
+    order, over their node window) and assembles it on its current CUDA
+    device with ``assemble_block_b200`` -- no inter-GPU traffic on the data
+    path.  The only collectives: an all-gather of the block nnz (global
+    offsets) and, with ``gather``, a gather of the blocks to ``root``, which
+    stitches them into the full matrices (bitwise the single-GPU result:
+    same contributions, same fold order)."""
+    import torch.distributed as dist
+
+    from .assembly import _as_descriptor, assemble_block_b200
+    from .kernels import restrict
+    from .mesh import Mesh
+
+    if dist.is_available() and dist.is_initialized():
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+    else:
+        world, rank = 1, 0
+    kernels = [_as_descriptor(mesh, k) for k in kernels]
+    m = kernels[0].m
+    nq = np.asarray(mesh.q).shape[1]
+    rb, re_ = row_blocks(nq, m, world)[rank]
+    sl = slab(mesh.q, mesh.me, m, rb, re_, getattr(mesh, "vols", None))
+    smesh = Mesh(sl.q, sl.me, sl.vols) if sl.vols is not None else Mesh.from_arrays(sl.q, sl.me)
+    window = slice(sl.node_lo, sl.node_lo + sl.q.shape[1])
+    skernels = [restrict(k, smesh, window, sl.elements) for k in kernels]
+    out = assemble_block_b200(smesh, skernels, sl.row_begin, sl.row_end, core=core, timings=timings,
+                              col_offset=sl.col_offset, ncols=m * nq)
+    blocks = [(rb, re_, b.row_ptr, b.col_idx, b.vals) for b in out]
+    offsets, totals, matrices = [], [], None
+    for b in out:
+        if world > 1:
+            off, tot, _ = global_offsets(b.nnz, group=group, device=_coll_device(group))
+        else:
+            off, tot = 0, b.nnz
+        offsets.append(off)
+        totals.append(tot)
+    if gather:
+        from .sparse import SparseMatrix
+
+        gathered = gather_blocks_to_root(blocks, group=group, root=root) if world > 1 else [blocks]
+        if rank == root:
+            matrices = []
+            for ki in range(len(kernels)):
+                rp, ci, va = stitch([g[ki] for g in gathered], m * nq, m * nq)
+                matrices.append(SparseMatrix(m * nq, m * nq, rp, ci, va))
+    return DistributedResult(rb, re_, blocks, offsets, totals, matrices)
+
+
+def _coll_device(group=None):
+    """Device for small collective tensors: the current CUDA device under
+    NCCL, the CPU under gloo."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")

@@ -50,6 +50,27 @@ def to_scipy(a: SparseMatrix):
     return scipy.sparse.csr_matrix((a.vals, a.col_idx, a.row_ptr), shape=(a.nrows, a.ncols))
 
 
+MM_HEADER = "%%MatrixMarket matrix coordinate real general"
+
+
+def write_matrixmarket(a: SparseMatrix, path, chunk: int = 1 << 20) -> None:
+    """MatrixMarket coordinate file, byte for byte the reference writer's
+    output (sparse.py:208-219: real general header, one-based indices, values
+    as ``%.17g``), formatted in chunks of ``chunk`` entries instead of one
+    Python f-string per entry."""
+    rp = np.asarray(a.row_ptr, dtype=np.int64)
+    ci = np.asarray(a.col_idx, dtype=np.int64)
+    va = np.asarray(a.vals, dtype=np.float64)
+    rows = np.repeat(np.arange(a.nrows, dtype=np.int64), np.diff(rp))
+    with open(path, "w") as f:
+        f.write(MM_HEADER + "\n")
+        f.write(f"{a.nrows} {a.ncols} {len(va)}\n")
+        for s in range(0, len(va), chunk):
+            e = min(s + chunk, len(va))
+            f.write("".join(f"{i} {j} {v:.17g}\n" for i, j, v in
+                            zip((rows[s:e] + 1).tolist(), (ci[s:e] + 1).tolist(), va[s:e].tolist())))
+
+
 def empty_matrix(nrows: int, ncols: int) -> SparseMatrix:
     return SparseMatrix(nrows, ncols, np.zeros(nrows + 1, dtype=np.int64),
                         np.empty(0, dtype=np.int64), np.empty(0, dtype=np.float64))

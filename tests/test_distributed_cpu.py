@@ -82,3 +82,68 @@ def test_two_rank_row_blocks_stitch_to_full_matrix(name, use_slab):
     results = [q.get(timeout=10) for _ in range(2)]
     assert all(results), results
     assert all(p.exitcode == 0 for p in procs)
+
+
+
+def _driver_worker(rank, world, port, name, result_q):
+    # the product's distributed driver (parallel.assemble_distributed): slab
+    # cut, coefficient restriction, offsets, gather, stitch -- with the block
+    # assembler swapped for the oracle (no GPU here; the -m gpu test runs the
+    # real one)
+    import sys
+
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch.distributed as dist
+
+    import paper_1401_3301_b200 as P
+    from conftest import device_kernel_for as dk, load_golden as lg, oracle_op_for as oo
+    from oracle import oracle as O
+    from paper_1401_3301_b200 import assembly, parallel
+
+    def fake_block(mesh, kernels, row_begin, row_end, core="SkylakeX", timings=None, col_offset=0, ncols=None):
+        out = []
+        for k in kernels:
+            g = {"q": mesh.q, "me": mesh.me, "vols": mesh.vols}
+            if k.op == "mass":
+                g["w"] = k.w if k.w is not None else np.full(mesh.q.shape[1], k.w_const)
+            if k.op == "elastic":
+                g["lamb"], g["mu"] = k.lamb, k.mu
+            if k.op == "general":
+                g.update(A=k.A, b=k.b, c=k.c, a0=k.a0)
+            ip, ix, va = O.assemble_block(mesh.q, mesh.me, oo(name, g), row_begin, row_end)
+            out.append(P.SparseMatrix(row_end - row_begin, ncols, ip, ix + col_offset, va))
+        return out
+
+    assembly.assemble_block_b200 = fake_block
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = lg(name)
+        mesh = P.Mesh(g["q"], g["me"], g["vols"])
+        res = parallel.assemble_distributed(mesh, [dk(name, g, mesh)])
+        if rank == 0:
+            a = res.matrices[0]
+            ok = (np.array_equal(a.row_ptr, g["row_ptr"]) and np.array_equal(a.col_idx, g["col_idx"])
+                  and np.array_equal(a.vals, g["vals"]) and res.totals[0] == len(g["vals"]) and res.offsets[0] == 0)
+            result_q.put(bool(ok))
+        else:
+            result_q.put(res.matrices is None and res.offsets[0] > 0)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["stiff_d3_n6_jit", "mass_d2_n15_jit", "elastic_d3_n6_jit", "general_d3_n6_jit"])
+def test_distributed_driver_two_ranks(name):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_driver_worker, args=(r, 2, port, name, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    results = [q.get(timeout=10) for _ in range(2)]
+    assert all(results), results
+    assert all(p.exitcode == 0 for p in procs)

@@ -559,3 +559,64 @@ def test_compute_sanitizer(cuda_ok, tool):
     assert r.returncode == 0, tail
     assert "sanitize case ok" in r.stdout, tail
     assert "ERROR SUMMARY: 0 errors" in r.stdout + r.stderr, tail
+
+
+
+def _dist_gpu_worker(rank, world, port, name, result_q):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    import torch
+    import torch.distributed as dist
+
+    import paper_1401_3301_b200 as P
+    from conftest import device_kernel_for as dk, load_golden as lg
+    from paper_1401_3301_b200 import device, parallel
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)   # one GPU here: both ranks on cuda:0, gloo collectives (functional check)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = lg(name)
+        mesh = P.Mesh(g["q"], g["me"], g["vols"])
+        device.launch_count(reset=True)
+        res = parallel.assemble_distributed(mesh, [dk(name, g, mesh)])
+        launched = device.launch_count()
+        if rank == 0:
+            a = res.matrices[0]
+            ok = (np.array_equal(a.row_ptr, g["row_ptr"]) and np.array_equal(a.col_idx, g["col_idx"])
+                  and np.array_equal(a.vals, g["vals"]) and res.totals[0] == len(g["vals"]) and launched > 0)
+            result_q.put(bool(ok))
+        else:
+            result_q.put(res.matrices is None and res.offsets[0] > 0 and launched > 0)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["stiff_d3_n8_jit", "general_d3_n8_jit", "elastic_d3_n6_jit", "mass_d2_n15_jit"])
+def test_distributed_driver_two_ranks_gpu(cuda_ok, name):
+    # parallel.assemble_distributed through the product block assembler on
+    # the GPU, two ranks (both on cuda:0 -- the pool has one GPU per call):
+    # slabs, per-rank symbolic + numeric, offsets, gather, stitch == the
+    # reference's matrix bitwise
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_dist_gpu_worker, args=(r, 2, port, name, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+    results = [q.get(timeout=10) for _ in range(2)]
+    assert all(results), results
+    assert all(p.exitcode == 0 for p in procs)

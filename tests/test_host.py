@@ -196,3 +196,34 @@ def test_kuhn_slab_window_covers_touching_elements(d, n, parts):
         used = me[:, e0:e1]
         assert used.size == 0 or (used.min() >= v0 and used.max() < v1)
         assert v0 <= rb and (re_ <= v1 or re_ == rb)
+
+
+def test_matrixmarket_writer_matches_reference(tmp_path):
+    # byte-for-byte the reference's write_matrixmarket (sparse.py:208-219)
+    import importlib
+    import sys
+
+    from oracle import oracle as O
+
+    ref = "/root/reference/pkg/src"
+    if not os.path.isdir(ref):
+        pytest.skip("reference tree not present (GPU box)")
+    q, me = P.hypercube_arrays(2, 6)
+    q = P.jitter_interior(q, 6, 0.2, 3)
+    vols = O.volumes(q, me)
+    rp, ci, va = O.assemble(q, me, O.OracleOp("stiffness", 2, vols))
+    va = va.copy()
+    va[3] = -1e-300
+    va[5] = 1.0 / 3.0
+    va[7] = 12345678901234567890.0
+    a = P.SparseMatrix(q.shape[1], q.shape[1], rp, ci, va)
+    P.write_matrixmarket(a, tmp_path / "ours.mtx", chunk=7)
+    sys.path.insert(0, ref)
+    try:
+        rs = importlib.import_module("simplex_asm.sparse")
+        rs.write_matrixmarket(rs.SparseMatrix(a.nrows, a.ncols, rp, ci, va), tmp_path / "ref.mtx")
+        assert (tmp_path / "ours.mtx").read_bytes() == (tmp_path / "ref.mtx").read_bytes()
+        back = rs.read_matrixmarket(tmp_path / "ours.mtx")
+        assert np.array_equal(back.vals, va) and np.array_equal(back.col_idx, ci)
+    finally:
+        sys.path.remove(ref)
