@@ -97,7 +97,8 @@ int sa_plan_info(const sa_plan *plan, int64_t *nrows, int64_t *nnz_structural,
 int sa_plan_pattern(const sa_plan *plan, int64_t *indptr_dev, int32_t *indices_dev, void *stream);
 /* Diagnostics: out[0..n) = {incidences, max row nodes, nodes, nnz, warp
  * interleaved records, two-pass slots, every element batch staged (0/1),
- * largest batch vertex count, device bytes of the plan's structures}. */
+ * largest batch vertex count, device bytes of the plan's structures,
+ * largest light-row degree, heavy rows (assembled by the hub kernel)}. */
 int sa_plan_stats(const sa_plan *plan, int64_t *out, int n);
 int sa_plan_destroy(sa_plan *plan);
 

@@ -84,6 +84,9 @@ struct sa_plan {
     // reference order by k_guard_fixup)
     uint32_t *gd_flag_rows = nullptr;
     int *gd_nflag = nullptr;
+    // heavy rows (degree above the light cap): assembled by k_heavy_rows
+    int64_t light_deg = 0, n_heavy = 0;
+    uint32_t *heavy_rows = nullptr;
 };
 
 // numeric-phase arguments (shared by the per-dimension translation units)
@@ -100,7 +103,7 @@ struct NumArgs {
     const int64_t *colptr;
     const int64_t *indptr;
     const int32_t *cols;  // node-level sorted neighbour nodes (row-gather coordinate cache)
-    int acc_stride;  // smem accumulator rows per output (m*m*max_deg)
+    int acc_stride;  // smem accumulator rows per output (m*m*light_deg)
     double *vals[2];
     int64_t *counters;
     // coefficients
@@ -126,6 +129,9 @@ struct NumArgs {
     int exact;       // general operator: reference-order (bitwise) element values
     int *nflag;          // fast general operator: guarded-row count + list
     uint32_t *flag_rows;
+    int light_deg;       // rows with more columns are heavy (k_heavy_rows), skipped by the row kernels
+    const uint32_t *heavy_rows;
+    int64_t n_heavy;
 };
 
 namespace {
@@ -249,7 +255,7 @@ template <int D>
 __global__ void k_node_cols(const typename IdxT<D>::type *__restrict__ me, const int64_t *__restrict__ inc_ptr,
                             const uint2 *__restrict__ inc, int64_t nnodes, int64_t *__restrict__ ncol,
                             const int64_t *__restrict__ colptr, int32_t *__restrict__ cols,
-                            unsigned long long *cap_flag)
+                            unsigned long long *nheavy, uint32_t *heavy)
 {
     int64_t nl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (nl >= nnodes) return;
@@ -270,12 +276,102 @@ __global__ void k_node_cols(const typename IdxT<D>::type *__restrict__ me, const
             ++n;
         }
     }
-    if (over) { atomicOr(cap_flag, 1ull); n = 0; }
+    if (over) {   // more than MAXC neighbours: k_heavy_cols builds this node's list
+        if (cols == nullptr) heavy[atomicAdd(nheavy, 1ull)] = (uint32_t)nl;
+        return;
+    }
     if (cols == nullptr) {
         ncol[nl] = n;
     } else {
         int64_t base = colptr[nl];
         for (int u = 0; u < n; ++u) cols[base + u] = buf[u];
+    }
+}
+
+
+// Nodes with more than MAXC distinct neighbours (k_node_cols' heavy list):
+// one CTA per node gathers the vertices of its incidences into shared
+// memory, bitonic-sorts them and keeps the unique ones (count, then fill).
+// Their incidence ranks are not used (heavy rows are assembled by
+// k_heavy_rows, which looks columns up in the sorted list).
+constexpr int HEAVY_CAP = 16384;   // vertex references (4 per 3D incidence) per heavy node
+template <int D>
+__global__ void __launch_bounds__(1024) k_heavy_cols(const typename IdxT<D>::type *__restrict__ me,
+                                                     const int64_t *__restrict__ inc_ptr, const uint2 *__restrict__ inc,
+                                                     const uint32_t *__restrict__ heavy, int64_t *__restrict__ ncol,
+                                                     const int64_t *__restrict__ colptr, int32_t *__restrict__ cols,
+                                                     unsigned long long *too_big)
+{
+    extern __shared__ int hk[];
+    __shared__ int s_part[32], s_n;
+    const uint32_t nl = heavy[blockIdx.x];
+    const int64_t t0 = inc_ptr[nl];
+    const int ni = (int)(inc_ptr[nl + 1] - t0);
+    const int nk = ni * (D + 1);
+    if (nk > HEAVY_CAP) {
+        if (threadIdx.x == 0) atomicOr(too_big, 1ull);
+        return;
+    }
+    int P = 1;
+    while (P < nk) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        int x = INT_MAX;
+        if (i < nk) {
+            int v[D + 1];
+            load_element<D>(me, inc[t0 + i / (D + 1)].x & 0x3fffffffu, v);
+            x = v[i % (D + 1)];
+        }
+        hk[i] = x;
+    }
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1)
+        for (int h = k >> 1; h > 0; h >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                const int p = i ^ h;
+                if (p > i) {
+                    const int a = hk[i], b = hk[p];
+                    if ((a > b) == ((i & k) == 0)) { hk[i] = b; hk[p] = a; }
+                }
+            }
+            __syncthreads();
+        }
+    // unique: heads among each thread's contiguous chunk, block scan of counts
+    const int per = (P + blockDim.x - 1) / blockDim.x;
+    const int c0 = threadIdx.x * per, c1 = min(c0 + per, nk);
+    int cnt = 0;
+    for (int i = c0; i < c1; ++i) cnt += (i == 0 || hk[i] != hk[i - 1]);
+    int incl = cnt;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int sh = 1; sh < 32; sh <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, sh);
+        if (lane >= sh) incl += y;
+    }
+    if (lane == 31) s_part[w] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int run = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { const int t = s_part[i]; s_part[i] = run; run += t; }
+        s_n = run;
+    }
+    __syncthreads();
+    if (cols == nullptr) {
+        if (threadIdx.x == 0) ncol[nl] = s_n;
+        return;
+    }
+    int pos = s_part[w] + incl - cnt;
+    const int64_t base = colptr[nl];
+    for (int i = c0; i < c1; ++i)
+        if (i == 0 || hk[i] != hk[i - 1]) cols[base + pos++] = hk[i];
+}
+
+// rows above the light-row degree cap (heavy rows), and the largest light degree
+__global__ void k_heavy_rows_list(const int64_t *__restrict__ colptr, int64_t nnodes, int64_t cap,
+                                  uint32_t *__restrict__ list, unsigned long long *__restrict__ cnt_max)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnodes; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t deg = colptr[i + 1] - colptr[i];
+        if (deg > cap) list[atomicAdd(cnt_max, 1ull)] = (uint32_t)i;
+        else atomicMax(cnt_max + 1, (unsigned long long)deg);
     }
 }
 
@@ -813,9 +909,11 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
     // row (odd, so lane strides hit distinct banks) and rows store their own
     // segments.
     const unsigned full = 0xffffffffu;
-    const bool active = nl < a.nnodes;
-    const int64_t c0 = active ? a.colptr[nl] : 0;
-    const int deg = active ? (int)(a.colptr[nl + 1] - c0) : -1;
+    const bool in_range = nl < a.nnodes;
+    const int64_t c0 = in_range ? a.colptr[nl] : 0;
+    const int deg_row = in_range ? (int)(a.colptr[nl + 1] - c0) : -1;
+    const bool active = in_range && deg_row <= a.light_deg;   // heavy rows: k_heavy_rows
+    const int deg = active ? deg_row : -1;
     // the row's CSR base, loaded with the degree (independent loads: one
     // round trip) rather than after the incidence loop
     const int64_t row_base = active ? a.indptr[M * nl] : 0;
@@ -1614,18 +1712,33 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
             fast = ov == 0;   // else (a node with > NS_CAPC neighbours): the general kernels below
         }
     }
+    uint32_t *hsym = nullptr;   // nodes with more than MAXC neighbours (general path)
+    int64_t nhsym = 0;
+    const size_t hsm = HEAVY_CAP * sizeof(int);
     if (nn && !fast) {
         SA_LAUNCH(k_inc_sort, grid_for(nn, 128), 128, 0, st, P->inc_ptr, nn, P->inc);
-        SA_CUDA_TRY(cudaMemsetAsync(P->counters + 5, 0, sizeof(int64_t), st));
+        SA_CUDA_TRY(cudaMallocAsync((void **)&hsym, nn * sizeof(uint32_t), st));
+        SA_CUDA_TRY(cudaMemsetAsync(P->counters + 5, 0, 2 * sizeof(int64_t), st));
         SA_LAUNCH(k_node_cols<D>, grid_for(nn, 128), 128, 0, st, (const I *)M->me, P->inc_ptr, P->inc, nn, cnt,
-                  (const int64_t *)nullptr, (int32_t *)nullptr, (unsigned long long *)(P->counters + 5));
+                  (const int64_t *)nullptr, (int32_t *)nullptr, (unsigned long long *)(P->counters + 5), hsym);
+        SA_CUDA_TRY(cudaMemcpyAsync(&nhsym, P->counters + 5, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        if (nhsym) {
+            SA_CUDA_TRY(cudaFuncSetAttribute(k_heavy_cols<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
+            SA_LAUNCH(k_heavy_cols<D>, (unsigned)nhsym, 1024, hsm, st, (const I *)M->me, P->inc_ptr, P->inc, hsym, cnt,
+                      (const int64_t *)nullptr, (int32_t *)nullptr, (unsigned long long *)(P->counters + 6));
+        }
     }
     SA_TRY(exclusive_scan_i64(cnt, P->colptr, nn, P->scan_tmp, st));
-    int64_t cap = 0;
+    int64_t too_big = 0;
     SA_CUDA_TRY(cudaMemcpyAsync(&P->n_colnodes, P->colptr + nn, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    if (!fast) SA_CUDA_TRY(cudaMemcpyAsync(&cap, P->counters + 5, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    if (nhsym) SA_CUDA_TRY(cudaMemcpyAsync(&too_big, P->counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     SA_CUDA_TRY(cudaStreamSynchronize(st));
-    if (cap) return set_error(SA_ERR_CAPACITY, "a node has more than %d distinct neighbours", MAXC);
+    if (too_big) {
+        SA_CUDA_TRY(cudaFreeAsync(hsym, st));
+        return set_error(SA_ERR_CAPACITY, "a node has more than %d vertex references in its incident elements",
+                         HEAVY_CAP);
+    }
     SA_CUDA_TRY(cudaMallocAsync((void **)&P->cols, std::max<int64_t>(P->n_colnodes, 1) * sizeof(int32_t), st));
     if (nn && fast) {
         SA_LAUNCH((k_node_symbolic<D, true>), grid_for(nn, NS_THREADS), NS_THREADS, 0, st, (const I *)M->me,
@@ -1633,10 +1746,14 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
                   (unsigned long long *)(P->counters + 7));
     } else if (nn) {
         SA_LAUNCH(k_node_cols<D>, grid_for(nn, 128), 128, 0, st, (const I *)M->me, P->inc_ptr, P->inc, nn, cnt,
-                  (const int64_t *)P->colptr, P->cols, (unsigned long long *)(P->counters + 5));
+                  (const int64_t *)P->colptr, P->cols, (unsigned long long *)nullptr, (uint32_t *)nullptr);
+        if (nhsym)
+            SA_LAUNCH(k_heavy_cols<D>, (unsigned)nhsym, 1024, hsm, st, (const I *)M->me, P->inc_ptr, P->inc, hsym, cnt,
+                      (const int64_t *)P->colptr, P->cols, (unsigned long long *)(P->counters + 6));
         SA_LAUNCH(k_inc_ranks<D>, grid_for(nn, 128), 128, 0, st, (const I *)M->me, P->inc_ptr, P->inc, nn, P->colptr,
                   P->cols);
     }
+    if (hsym) SA_CUDA_TRY(cudaFreeAsync(hsym, st));
     // max node degree: device reduction (no host copy of colptr)
     SA_CUDA_TRY(cudaMemsetAsync(P->counters + 6, 0, sizeof(int64_t), st));
     if (nn)
@@ -1647,6 +1764,28 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
     SA_CUDA_TRY(cudaStreamSynchronize(st));
     P->max_deg = md;
     const int m = P->m;
+    // light / heavy rows: the row kernels size their shared-memory
+    // accumulators for the light rows only; rows above the cap (hubs) are
+    // assembled by k_heavy_rows, so one hub neither shrinks every block nor
+    // runs into the 8-bit column ranks
+    {
+        const int64_t avg = nn ? (P->n_colnodes + nn - 1) / nn : 0;
+        const int64_t smem_cap = m == 1 ? 200 : (m == 2 ? 100 : 44);
+        const int64_t cap = std::min<int64_t>(std::min<int64_t>(smem_cap, MAXC), std::max<int64_t>(2 * avg + 8, 16));
+        P->light_deg = md;
+        P->n_heavy = 0;
+        if (md > cap) {
+            SA_CUDA_TRY(cudaMallocAsync((void **)&P->heavy_rows, nn * sizeof(uint32_t), st));
+            SA_CUDA_TRY(cudaMemsetAsync(P->counters + 6, 0, 2 * sizeof(int64_t), st));
+            SA_LAUNCH(k_heavy_rows_list, std::min<int64_t>(grid_for(nn, 256), 148 * 8), 256, 0, st, P->colptr, nn, cap,
+                      P->heavy_rows, (unsigned long long *)(P->counters + 6));
+            int64_t h[2];
+            SA_CUDA_TRY(cudaMemcpyAsync(h, P->counters + 6, sizeof h, cudaMemcpyDeviceToHost, st));
+            SA_CUDA_TRY(cudaStreamSynchronize(st));
+            P->n_heavy = h[0];
+            P->light_deg = h[1];
+        }
+    }
     P->nnz = (int64_t)m * m * P->n_colnodes;
     if (P->nnz >= ((int64_t)1 << 31) || (int64_t)m * M->nq >= ((int64_t)1 << 31))
         return set_error(SA_ERR_CAPACITY, "block has %lld structural entries; int32 column indices overflow",
@@ -1814,12 +1953,73 @@ int launch_twopass(const sa_plan *P, const NumArgs &a, int64_t nnodes, cudaStrea
     return SA_OK;
 }
 
+
+// Heavy rows (degree above the plan's light cap): one thread per row, exact
+// element values (element_krow, reference order) folded in ascending element
+// order straight into the row's CSR segment in global memory; the column of
+// each element vertex is looked up in the row's sorted column list (ranks
+// may exceed 8 bits).  Bitwise the row-gather result; zeros counted.
+template <int D, int M, int OPS, int CORE>
+__global__ void k_heavy_rows(NumArgs a)
+{
+    constexpr int NOUT = n_outputs<OPS>();
+    constexpr int MM = M * M;
+    int nz[NOUT];
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o) nz[o] = 0;
+    int64_t emin = INT64_MAX;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n_heavy;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t nl = a.heavy_rows[i];
+        const int64_t c0 = a.colptr[nl];
+        const int deg = (int)(a.colptr[nl + 1] - c0);
+        for (int o = 0; o < NOUT; ++o)
+            for (int l = 0; l < M; ++l) {
+                const int64_t p = a.indptr[M * nl + l];
+                for (int k = 0; k < M * deg; ++k) a.vals[o][p + k] = 0.0;
+            }
+        for (int64_t t = a.inc_ptr[nl]; t < a.inc_ptr[nl + 1]; ++t) {
+            const uint2 rec = a.inc[t];
+            const int64_t e = rec.x & 0x3fffffffu;
+            ElemRaw<D> x;
+            element_load1<D, OPS>(a, e, x);
+            element_load2<D, OPS>(a, x);
+            ElemGeo<D> g;
+            if (element_compute<D, OPS, CORE>(x, g)) emin = min(emin, e);
+            double vals[(D + 1) * NOUT * MM];
+            krow_runtime<D, M, OPS>(a, g, rec.x >> 30, vals);
+            for (int b = 0; b <= D; ++b) {
+                int lo = 0, hi = deg;
+                while (lo < hi) { const int mid = (lo + hi) >> 1; if (a.cols[c0 + mid] < x.v[b]) lo = mid + 1; else hi = mid; }
+                for (int o = 0; o < NOUT; ++o)
+                    for (int l = 0; l < M; ++l) {
+                        const int64_t p = a.indptr[M * nl + l] + (int64_t)lo * M;
+                        for (int n = 0; n < M; ++n) a.vals[o][p + n] += vals[(b * NOUT + o) * MM + l * M + n];
+                    }
+            }
+        }
+        for (int o = 0; o < NOUT; ++o)
+            for (int l = 0; l < M; ++l) {
+                const int64_t p = a.indptr[M * nl + l];
+                for (int k = 0; k < M * deg; ++k) nz[o] += (a.vals[o][p + k] == 0.0);
+            }
+    }
+    if (emin != INT64_MAX) atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)emin);
+#pragma unroll
+    for (int o = 0; o < NOUT; ++o)
+        if (nz[o]) atomicAdd((unsigned long long *)(a.counters + o), (unsigned long long)nz[o]);
+}
+
 template <int D, int M, int OPS, int CORE>
 int launch_numeric(const sa_plan *P, const NumArgs &a, cudaStream_t st)
 {
-    if (a.kbuf) return launch_twopass<D, M, OPS, CORE>(P, a, P->nnodes, st);
-    return launch_rowgather<D, M, OPS, CORE>(a, P->nnodes, st);
+    if (a.kbuf) SA_TRY((launch_twopass<D, M, OPS, CORE>(P, a, P->nnodes, st)));
+    else SA_TRY((launch_rowgather<D, M, OPS, CORE>(a, P->nnodes, st)));
+    if (a.n_heavy)
+        SA_LAUNCH((k_heavy_rows<D, M, OPS, CORE>), (unsigned)std::min<int64_t>(grid_for(a.n_heavy, 64), 148), 64, 0, st, a);
+    return SA_OK;
 }
+
 
 template <int D, int M, int OPS>
 int launch_numeric_core(const sa_plan *P, const NumArgs &a, int core, cudaStream_t st)
@@ -1987,7 +2187,7 @@ int sa_plan_destroy(sa_plan *P)
     if (!P) return SA_OK;
     free_all({P->inc_ptr, P->inc, P->winc, P->wseg, P->colptr, P->cols, P->indptr, P->indices, P->counters,
               P->scan_tmp, P->epos, P->kbuf, P->tp_rank, P->eb_verts, P->eb_count, P->eb_loc, P->gd_flag_rows,
-              P->gd_nflag});
+              P->gd_nflag, P->heavy_rows});
     delete P;
     return SA_OK;
 }
@@ -2046,9 +2246,9 @@ int sa_plan_stats(const sa_plan *P, int64_t *out, int n)
                           P->n_winc * (int64_t)sizeof(IncRec) + (P->wseg ? (nw + 1) * 8 : 0) +
                           (P->epos ? ne * 16 : 0) + P->kbuf_elems * 8 + P->tp_nslots * 4 +
                           (P->eb_loc ? ne * 4 + nb * (EB_CAP + 1) * 4 : 0);
-    const int64_t v[9] = {P->n_inc, P->max_deg, P->nnodes, P->nnz, P->n_winc, P->tp_nslots, P->eb_allfit ? 1 : 0,
-                          P->eb_maxn, bytes};
-    for (int i = 0; i < n && i < 9; ++i) out[i] = v[i];
+    const int64_t v[11] = {P->n_inc, P->max_deg, P->nnodes, P->nnz, P->n_winc, P->tp_nslots, P->eb_allfit ? 1 : 0,
+                           P->eb_maxn, bytes, P->light_deg, P->n_heavy};
+    for (int i = 0; i < n && i < 11; ++i) out[i] = v[i];
     return SA_OK;
 }
 
@@ -2191,7 +2391,10 @@ int sa_numeric(sa_plan *P, int ops, const sa_coeffs *cf, double *const *vals_dev
     a.qv = M->qv; a.me = M->me; a.vols = M->vols;
     a.nnodes = P->nnodes; a.node_begin = P->node_begin;
     a.inc_ptr = P->inc_ptr; a.inc = P->inc; a.winc = P->winc; a.wseg = P->wseg; a.colptr = P->colptr; a.indptr = P->indptr; a.cols = P->cols;
-    a.acc_stride = (int)(P->m * P->m * std::max<int64_t>(P->max_deg, 1));
+    a.acc_stride = (int)(P->m * P->m * std::max<int64_t>(P->light_deg, 1));
+    a.light_deg = (int)P->light_deg;
+    a.heavy_rows = P->heavy_rows;
+    a.n_heavy = P->n_heavy;
     int nout = 0;
     for (int bit = 1; bit <= 8; bit <<= 1)
         if (ops & bit) { a.vals[nout] = vals_dev[nout]; ++nout; }

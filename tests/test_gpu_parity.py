@@ -263,9 +263,11 @@ def test_unstructured_delaunay_mesh(cuda_ok, kernel, monkeypatch):
         assert_csr_equal(mass, *_oracle(mesh, "mass", nthreads=4, w=1.0 + mesh.q[0]))
 
 
-@pytest.mark.parametrize("k", [40, 70])
+@pytest.mark.parametrize("k", [40, 70, 400])
 def test_high_valence_node(cuda_ok, k):
-    # a fan of k triangles around node 0 (k incidences, k+1 neighbours)
+    # a fan of k triangles around node 0 (k incidences, k+1 neighbours; 400:
+    # beyond the 8-bit column ranks -- the reference has no valence limit,
+    # sparse.py:85-115)
     from oracle import oracle as O
 
     ang = np.linspace(0, 2 * np.pi, k, endpoint=False)
@@ -620,3 +622,42 @@ def test_distributed_driver_two_ranks_gpu(cuda_ok, name):
     results = [q.get(timeout=10) for _ in range(2)]
     assert all(results), results
     assert all(p.exitcode == 0 for p in procs)
+
+
+
+@pytest.mark.parametrize("kind", ["elastic", "stiffness", "general"])
+def test_3d_hub_node(cuda_ok, kind):
+    # a hub node joined to 120 points on a sphere (cone over the convex hull):
+    # its rows are heavy (k_heavy_rows), the other rows keep small
+    # accumulators; bitwise against the oracle
+    from scipy.spatial import ConvexHull
+
+    from oracle import oracle as O
+    from paper_1401_3301_b200.device import DeviceMesh
+
+    rng = np.random.default_rng(7)
+    p = rng.standard_normal((120, 3))
+    p /= np.linalg.norm(p, axis=1)[:, None]
+    hull = ConvexHull(p)
+    q = np.ascontiguousarray(np.vstack([np.zeros((1, 3)), p]).T)
+    tri = hull.simplices + 1
+    me = np.ascontiguousarray(np.vstack([np.zeros(len(tri), dtype=np.int64), tri.T.astype(np.int64)]))
+    mesh = P.Mesh(q, me, O.volumes(q, me))
+    nq = q.shape[1]
+    if kind == "elastic":
+        lam, mu = 1.0 + q[0] ** 2, 0.5 + 0.1 * q[1]
+        got = P.assemble_vector_b200(mesh, P.ElasticKernel(mesh, lam, mu))
+        ref = _oracle(mesh, "elastic", nthreads=2, lamb=lam, mu=mu)
+        m = 3
+    elif kind == "stiffness":
+        got = P.assemble_b200(mesh, P.StiffnessKernel(mesh))
+        ref = _oracle(mesh, "stiffness", nthreads=2)
+        m = 1
+    else:
+        f = _c5_fields(nq, 3)
+        got = P.assemble_b200(mesh, P.GeneralKernel(mesh, exact=True, **f))
+        ref = _oracle(mesh, "general", nthreads=2, **f)
+        m = 1
+    assert_csr_equal(got, *ref)
+    st = DeviceMesh(mesh.q, mesh.me, mesh.vols).plan(m).stats()
+    assert st["max_row_nodes"] == 121 and st["heavy_rows"] == 1 and st["light_row_nodes"] < 40, st
