@@ -176,30 +176,29 @@ def assemble_block_b200(mesh, kernels, row_begin: int, row_end: int, core: str =
 
     kernels = [_as_descriptor(mesh, k) for k in kernels]
     t = time.perf_counter()
-    # connectivity first (the symbolic phase needs only it); the coordinates
-    # and volumes upload on a side stream while the symbolic phase runs
-    # (and volumes: the 3D records carry them)
+    # connectivity and volumes first (the symbolic phase needs the former;
+    # uploading the volumes on the side stream instead measured slower: C5
+    # e2e 315 vs 215 ms); coordinates and coefficients follow on a side
+    # stream while the symbolic phase runs
     main = torch.cuda.current_stream()
     med = torch.as_tensor(np.asarray(mesh.me)).to(main.device, non_blocking=True)
     vols = getattr(mesh, "vols", None)
+    vd = torch.as_tensor(np.asarray(vols)).to(main.device, non_blocking=True) if vols is not None else None
     me_done = torch.cuda.Event()
     me_done.record(main)
     side = torch.cuda.Stream(device=main.device)
     side.wait_event(me_done)
     with torch.cuda.stream(side):
-        # coordinates, volumes and coefficients follow the connectivity on
-        # the side stream; the symbolic phase (connectivity only) overlaps them
         qd = torch.as_tensor(np.asarray(mesh.q)).to(main.device, non_blocking=True)
-        vd = torch.as_tensor(np.asarray(vols)).to(main.device, non_blocking=True) if vols is not None else None
     # nodal coefficients (pinned copies cached on the descriptors) upload on
     # the side stream too, behind the coordinates, during the symbolic phase
     order = sorted(kernels, key=lambda k: OP_BITS[k.op])
     coeffs = upload_coeffs(order, main.device, int(np.asarray(mesh.q).shape[0]), side)
-    dm = DeviceMesh(None, med, None, core=core, nq=int(np.asarray(mesh.q).shape[1]))
+    dm = DeviceMesh(None, med, vd, core=core, nq=int(np.asarray(mesh.q).shape[1]))
     t1 = time.perf_counter()
     plan = dm.plan(kernels[0].m, row_begin, row_end)
     main.wait_stream(side)
-    dm.set_coords(qd, vd)
+    dm.set_coords(qd)
     # the structural pattern downloads while the numeric phase runs
     pat = _PatternDownload(*plan.pattern(), col_offset, kernels[0].m * dm.nq)
     t2 = time.perf_counter()

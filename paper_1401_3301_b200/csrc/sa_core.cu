@@ -1222,7 +1222,27 @@ __global__ void __launch_bounds__(128, MINB) k_element_rows(NumArgs a)
 // load destinations, so more warps fit and the fp64 pipe stays fed.
 constexpr int EB_SIZE = 128;   // elements per batch
 constexpr int EB_CAP = 255;    // distinct vertices per batch (8-bit local ids)
-constexpr int EB_REC = 20;     // staged doubles per vertex: q (4, padded) + [A(9) b(3) c(3) a0]
+// staged doubles per vertex: q (4, padded) + [A(9) b(3) c(3) a0] + 2 pad: a
+// 176-byte stride = 11 x 16 B (odd), so the 128-bit shared loads of lanes
+// reading different vertices spread over the banks (the 160-byte stride put
+// every 4th vertex on the same bank group: L1 at 81 % of peak in C5)
+constexpr int EB_REC = 22;
+
+// one staged vertex record as 10 x 128-bit shared loads: c[0..3] = q (padded), w[0..15]
+__device__ __forceinline__ void stage_record(const double *__restrict__ rec, double (&c)[4], double (&w)[16])
+{
+    const double2 *r2 = reinterpret_cast<const double2 *>(rec);
+    double2 t = r2[0];
+    c[0] = t.x; c[1] = t.y;
+    t = r2[1];
+    c[2] = t.x; c[3] = t.y;
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+        t = r2[2 + h];
+        w[2 * h] = t.x;
+        w[2 * h + 1] = t.y;
+    }
+}
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
 {
@@ -1318,10 +1338,10 @@ __device__ __forceinline__ void element_from_stage(const double *__restrict__ vr
 {
 #pragma unroll
     for (int k = 0; k <= D; ++k) {
-        const double *rec = vrec + ((lc >> (8 * k)) & 0xff) * EB_REC;
+        double cq[4], w[16];
+        stage_record(vrec + ((lc >> (8 * k)) & 0xff) * EB_REC, cq, w);
 #pragma unroll
-        for (int c = 0; c < D; ++c) r.x[k][c] = rec[c];
-        const double *w = rec + 4;
+        for (int c = 0; c < D; ++c) r.x[k][c] = cq[c];
 #pragma unroll
         for (int ii = 0; ii < D; ++ii) {
 #pragma unroll
@@ -1349,17 +1369,20 @@ template <int D, int CORE>
 __device__ __forceinline__ bool stage_general_fast(const NumArgs &a, const double *__restrict__ vrec, unsigned lc,
                                                    double vol, const unsigned (&pos)[4])
 {
-    const double *rk[D + 1];
+    const double2 *rk[D + 1];   // records as 16-byte words (EB_REC even, 16 B aligned)
 #pragma unroll
-    for (int k = 0; k <= D; ++k) rk[k] = vrec + ((lc >> (8 * k)) & 0xff) * EB_REC;
+    for (int k = 0; k <= D; ++k) rk[k] = reinterpret_cast<const double2 *>(vrec + ((lc >> (8 * k)) & 0xff) * EB_REC);
     double G[D + 1][D];
     bool deg;
     {
         double x[D + 1][D];
 #pragma unroll
-        for (int k = 0; k <= D; ++k)
+        for (int k = 0; k <= D; ++k) {
+            const double2 t0 = rk[k][0], t1 = rk[k][1];
+            const double c4[4] = {t0.x, t0.y, t1.x, t1.y};
 #pragma unroll
-            for (int c = 0; c < D; ++c) x[k][c] = rk[k][c];
+            for (int c = 0; c < D; ++c) x[k][c] = c4[c];
+        }
         deg = element_gradients<D, CORE>(x, G);
     }
     const double s1 = vol * (1.0 / (D + 1));
@@ -1368,7 +1391,13 @@ __device__ __forceinline__ bool stage_general_fast(const NumArgs &a, const doubl
     double As[D][D], bs[D], cs[D], a0s;
 #pragma unroll
     for (int k = 0; k <= D; ++k) {
-        const double *w = rk[k] + 4;
+        double w[16];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+            const double2 t = rk[k][2 + h];
+            w[2 * h] = t.x;
+            w[2 * h + 1] = t.y;
+        }
 #pragma unroll
         for (int i = 0; i < D; ++i) {
 #pragma unroll
@@ -1388,20 +1417,22 @@ __device__ __forceinline__ bool stage_general_fast(const NumArgs &a, const doubl
     double Rv[D + 1][D], ea[D + 1], a0v[D + 1];
 #pragma unroll
     for (int k = 0; k <= D; ++k) {
-        const double *w = rk[k] + 4;
+        const double2 t6 = rk[k][8], t7 = rk[k][9];   // w[12..15] = c (3) | a0
+        const double cw[3] = {t6.x, t6.y, t7.x};
 #pragma unroll
-        for (int i = 0; i < D; ++i) Rv[k][i] = __fma_rn(s2, w[12 + i], cs[i]);
-        a0v[k] = w[15];
-        ea[k] = a0s + w[15];
+        for (int i = 0; i < D; ++i) Rv[k][i] = __fma_rn(s2, cw[i], cs[i]);
+        a0v[k] = t7.y;
+        ea[k] = a0s + t7.y;
     }
     double K[D + 1][D + 1];
 #pragma unroll
     for (int b = 0; b <= D; ++b) {
-        const double *w = rk[b] + 4;
+        const double2 t4 = rk[b][6], t5 = rk[b][7];   // w[8..11]: w[9..11] = b
+        const double bw[3] = {t4.y, t5.x, t5.y};
         double Q[D];
 #pragma unroll
         for (int i = 0; i < D; ++i) {
-            double t = __fma_rn(-s2, w[9 + i], bs[i]);
+            double t = __fma_rn(-s2, bw[i], bs[i]);
 #pragma unroll
             for (int j = 0; j < D; ++j) t = __fma_rn(As[i][j], G[b][j], t);
             Q[i] = t;

@@ -18,7 +18,7 @@ os.makedirs(dst, exist_ok=True)
 for p in glob.glob(os.path.join(src, f"ncu_*_{tag}.json")) + glob.glob(os.path.join(src, f"launches_*_{tag}.csv")):
     shutil.copy(p, dst)
 lines = []
-for name in ("C2", "C1", "C3", "C4", "C5", "ref"):
+for name in ("C5", "C1", "C2", "C3", "C4", "ref"):
     p = os.path.join(src, f"ev_bench_{name}.log")
     if not os.path.exists(p):
         continue
@@ -39,4 +39,6 @@ with open(os.path.join(dst, "bench_lines.jsonl"), "w") as f:
 par = [ln for ln in open(os.path.join(src, "ev_fullsize_parity.log")).read().splitlines() if ln.startswith("{")]
 with open(os.path.join(dst, "fullsize_parity.jsonl"), "w") as f:
     f.write("\n".join(par) + "\n")
+for p in glob.glob(os.path.join(src, "bench_table_*.csv")):
+    shutil.copy(p, dst)
 print(f"{len(lines)} bench lines, {len(par)} parity lines -> {dst}")
