@@ -1220,7 +1220,7 @@ __global__ void __launch_bounds__(128, MINB) k_element_rows(NumArgs a)
 // tetrahedra, so a batch of 128 consecutive elements of a Kuhn mesh needs
 // ~90 records instead of 512 register gathers; the compute phase holds no
 // load destinations, so more warps fit and the fp64 pipe stays fed.
-constexpr int EB_SIZE = 128;   // elements per batch
+constexpr int EB_SIZE = 256;   // elements per batch (C5: ~150 distinct vertices staged per batch)
 constexpr int EB_CAP = 255;    // distinct vertices per batch (8-bit local ids)
 // staged doubles per vertex: q (4, padded) + [A(9) b(3) c(3) a0] + 2 pad: a
 // 176-byte stride = 11 x 16 B (odd), so the 128-bit shared loads of lanes
@@ -1952,8 +1952,9 @@ int launch_twopass(const sa_plan *P, const NumArgs &a, int64_t nnodes, cudaStrea
     const bool fast = pipe && !a.exact;
     if constexpr (GEN3) {
         if (pipe) {
-            // (fast: 126 registers, 4 blocks/SM -- C5 7.89 vs 8.05 ms at 3)
-            auto pk = fast ? k_element_rows_pipe<D, M, OPS, CORE, 4, true> : k_element_rows_pipe<D, M, OPS, CORE, 3>;
+            // (fast: 126 registers, 2 blocks of 256 per SM; batches of 256
+            // elements read 7.7 instead of 9.5 GB -- C5 7.77 vs 7.90 ms)
+            auto pk = fast ? k_element_rows_pipe<D, M, OPS, CORE, 2, true> : k_element_rows_pipe<D, M, OPS, CORE, 1>;
             const size_t psm = 2 * (size_t)std::max(a.eb_maxn, 1) * EB_REC * sizeof(double) +
                                3 * (EB_CAP + 1) * sizeof(int);
             SA_CUDA_TRY(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
