@@ -661,3 +661,56 @@ def test_3d_hub_node(cuda_ok, kind):
     assert_csr_equal(got, *ref)
     st = DeviceMesh(mesh.q, mesh.me, mesh.vols).plan(m).stats()
     assert st["max_row_nodes"] == 121 and st["heavy_rows"] == 1 and st["light_row_nodes"] < 40, st
+
+
+
+@pytest.mark.parametrize("core", ["SkylakeX", "Haswell"])
+def test_general_fast_unstructured_and_cores(cuda_ok, core):
+    # the fast general operator on an unstructured Delaunay tet mesh (valence
+    # 10-30, irregular element batches) under both OpenBLAS kernel families:
+    # pattern exact, values within 1e-12 of the row max; exact mode bitwise
+    from scipy.spatial import Delaunay
+
+    from oracle import oracle as O
+    from paper_1401_3301_b200.assembly import to_host
+    from paper_1401_3301_b200.device import DeviceMesh
+
+    rng = np.random.default_rng(11)
+    pts = rng.random((3000, 3))
+    me = np.ascontiguousarray(Delaunay(pts).simplices.T.astype(np.int64))
+    q = np.ascontiguousarray(pts.T)
+    vols = O.volumes(q, me)
+    me = np.ascontiguousarray(me[:, vols > 1e-9])
+    mesh = P.Mesh(q, me, O.volumes(q, me))
+    f = _c5_fields(q.shape[1], 12)
+    op = O.OracleOp("general", 3, mesh.vols, core=core, **f)
+    rp, ci, va = O.assemble(q, mesh.me, op, nthreads=8)
+    for exact in (False, True):
+        plan = DeviceMesh(mesh.q, mesh.me, mesh.vols, core=core).plan(1)
+        (csr,) = plan.assemble([P.GeneralKernel(mesh, exact=exact, **f)])
+        assert_csr_equal(to_host(csr), rp, ci, va, bitwise=exact)
+
+
+def test_general_fast_row_blocks_stitch(cuda_ok):
+    # fast general operator on row-block slabs (parallel.slab: local node
+    # window, shifted columns, coefficient windows) stitches to the full
+    # oracle matrix within north_star's bar, pattern exact
+    from oracle import oracle as O
+    from paper_1401_3301_b200 import kernels as K
+    from paper_1401_3301_b200 import parallel
+    from paper_1401_3301_b200.assembly import assemble_block_b200
+
+    mesh = _jittered(3, 12, 31)
+    nq = mesh.q.shape[1]
+    f = _c5_fields(nq, 31)
+    full = P.GeneralKernel(mesh, **f)
+    blocks = []
+    for rb, re_ in parallel.row_blocks(nq, 1, 3):
+        sl = parallel.slab(mesh.q, mesh.me, 1, rb, re_, mesh.vols)
+        smesh = P.Mesh(sl.q, sl.me, sl.vols)
+        kk = K.restrict(full, smesh, slice(sl.node_lo, sl.node_lo + sl.q.shape[1]), sl.elements)
+        (b,) = assemble_block_b200(smesh, [kk], sl.row_begin, sl.row_end, col_offset=sl.col_offset, ncols=nq)
+        assert b.ncols == nq
+        blocks.append((rb, re_, b.row_ptr, b.col_idx, b.vals))
+    rp, ci, va = parallel.stitch(blocks, nq, nq)
+    assert_csr_equal(P.SparseMatrix(nq, nq, rp, ci, va), *_oracle(mesh, "general", **f), bitwise=False)
