@@ -137,7 +137,7 @@ def make_kernels(cfg, mesh, window=None):
             f = general_coeffs(cfg, nq)
             if window is not None:
                 f = {k: np.ascontiguousarray(v[window[0]:window[0] + mesh.q.shape[1]]) for k, v in f.items()}
-            out.append(P.GeneralKernel(mesh, **f))
+            out.append(P.GeneralKernel(mesh, exact=os.environ.get("SA_BENCH_EXACT") == "1", **f))
     return out
 
 

@@ -1954,7 +1954,7 @@ int launch_twopass(const sa_plan *P, const NumArgs &a, int64_t nnodes, cudaStrea
         if (pipe) {
             // (fast: 126 registers, 2 blocks of 256 per SM; batches of 256
             // elements read 7.7 instead of 9.5 GB -- C5 7.77 vs 7.90 ms)
-            auto pk = fast ? k_element_rows_pipe<D, M, OPS, CORE, 2, true> : k_element_rows_pipe<D, M, OPS, CORE, 1>;
+            auto pk = fast ? k_element_rows_pipe<D, M, OPS, CORE, 2, true> : k_element_rows_pipe<D, M, OPS, CORE, 2>;
             const size_t psm = 2 * (size_t)std::max(a.eb_maxn, 1) * EB_REC * sizeof(double) +
                                3 * (EB_CAP + 1) * sizeof(int);
             SA_CUDA_TRY(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
