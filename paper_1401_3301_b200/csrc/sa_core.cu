@@ -13,6 +13,7 @@
 // No atomics touch values: the output is deterministic by construction.
 #include <algorithm>
 #include <climits>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -87,6 +88,16 @@ struct sa_plan {
     // heavy rows (degree above the light cap): assembled by k_heavy_rows
     int64_t light_deg = 0, n_heavy = 0;
     uint32_t *heavy_rows = nullptr;
+    // tiled two-pass (sa_tiles.cuh): rows grouped into spatial tiles whose
+    // local rows fit the L2; per tile the touching elements (virtual element
+    // list, batch-aligned) and tile-relative slots into a reused ring buffer
+    bool tiled = false, tile_tried = false;
+    int64_t nt = 0, nv = 0, tile_max_slots = 0;
+    std::vector<int64_t> tile_w0, tile_v0;   // (nt+1) sorted-warp / virtual-element range of each tile
+    uint32_t *tw_order = nullptr;   // (nw) the warp (of 32 node rows) at each sorted position
+    int64_t *tw_vseg = nullptr;     // (nw+1) virtual slot offset of each sorted position
+    int32_t *tv_elem = nullptr;     // (nv) element of each virtual element, -1 = padding
+    uint4 *tv_pos = nullptr;        // (nv) tile-relative slots of its 4 local rows, ~0u = row outside the tile
 };
 
 // numeric-phase arguments (shared by the per-dimension translation units)
@@ -132,6 +143,12 @@ struct NumArgs {
     int light_deg;       // rows with more columns are heavy (k_heavy_rows), skipped by the row kernels
     const uint32_t *heavy_rows;
     int64_t n_heavy;
+    // tiled two-pass: virtual element list (element pass), sorted warp
+    // positions [tw_p0, tw_p1) of the tile (fold)
+    const int32_t *elist;
+    const uint32_t *tw_order;
+    const int64_t *tw_vseg;
+    int64_t tw_p0, tw_p1;
 };
 
 namespace {
@@ -890,9 +907,11 @@ __device__ __forceinline__ void krow_runtime(const NumArgs &a, const ElemGeo<D> 
 // accumulators indexed by the 8-bit column ranks stored with each incidence.
 // Used when a node has more than 31 incidences or the block kernel's shared
 // memory does not fit.
-template <int D, int M, int OPS, int CORE, int ILP, int MINB, bool PRE = false, bool LEAN = false, bool GUARD = false>
+template <int D, int M, int OPS, int CORE, int ILP, int MINB, bool PRE = false, bool LEAN = false, bool GUARD = false,
+          bool TILED = false>
 __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
 {
+    static_assert(!TILED || PRE, "tiles serve the two-pass fold only");
     // LEAN: a constant mass weight, known at compile time (the local copy is
     // scalar-replaced; w == nullptr folds the weight loads away)
     NumArgs a = a_in;
@@ -900,7 +919,14 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
     constexpr int NOUT = n_outputs<OPS>();
     extern __shared__ double smem_acc[];
     const int tid = threadIdx.x, lane = tid & 31;
-    const int64_t nl = blockIdx.x * (int64_t)blockDim.x + tid;
+    // TILED: the block's warps are sorted positions tw_p0 + ... of the tile;
+    // position p holds the 32 node rows of warp tw_order[p]
+    int64_t nl = blockIdx.x * (int64_t)blockDim.x + tid;
+    int64_t tpos = 0;
+    if constexpr (TILED) {
+        tpos = a.tw_p0 + (nl >> 5);
+        nl = tpos < a.tw_p1 ? (int64_t)a.tw_order[tpos] * 32 + lane : a.nnodes;
+    }
     // Accumulators: per warp and output a plane of 32 lane rows of S doubles;
     // lane j's dof row l, column k at wacc[o*32*S + j*S + l*M*deg + k].  When
     // the warp's rows all have degree d0, S = M*M*d0 and the plane IS the
@@ -997,10 +1023,16 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
             // the warp at wseg + 32 k + j, so each warp load is one contiguous
             // run); ranks and rows are independent loads -- no gather chain,
             // U incidences in flight
-            const int64_t sb = a.wseg[nl >> 5] + lane;
+            // (TILED: ranks in virtual slot order, rows in the tile's ring
+            // buffer at tile-relative slots -- L2 hits, default policy)
+            const int64_t sb = TILED ? a.tw_vseg[tpos] + lane : a.wseg[nl >> 5] + lane;
+            const int64_t kofs = TILED ? a.tw_vseg[a.tw_p0] : 0;
             auto loadk = [&](int64_t slot, double(&v)[VPR]) {
-                const double *src = a.kbuf + slot * a.kstride;
-                if constexpr (VPR % 4 == 0) {
+                const double *src = a.kbuf + (slot - kofs) * a.kstride;
+                if constexpr (VPR % 4 == 0 && TILED) {
+#pragma unroll
+                    for (int i = 0; i < VPR; i += 4) ldg256(src + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+                } else if constexpr (VPR % 4 == 0) {
 #pragma unroll
                     for (int i = 0; i < VPR; i += 4) ldg256_cs(src + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
                 } else if constexpr (VPR % 2 == 0) {
@@ -1098,7 +1130,8 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
 #pragma unroll
             for (int o = 0; o < NOUT; ++o) {
                 const double val = plane[o * 32 * S + i];
-                a.vals[o][base + i] = val;
+                if constexpr (TILED) __stcs(a.vals[o] + base + i, val);   // streamed: keep the ring in L2
+                else a.vals[o][base + i] = val;
                 if constexpr (!GUARD) nz[o] += (val == 0.0);
             }
         }
@@ -1146,10 +1179,14 @@ __device__ __forceinline__ void st256_cs(double *p, double a, double b, double c
     asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
 
-template <int VPR>
+// KEEP: default cache policy (tiled two-pass: the fold reads the row back from L2)
+template <int VPR, bool KEEP = false>
 __device__ __forceinline__ void store_row(double *dst, const double (&vals)[VPR])
 {
-    if constexpr (VPR % 4 == 0) {
+    if constexpr (VPR % 4 == 0 && KEEP) {
+#pragma unroll
+        for (int i = 0; i < VPR; i += 4) st256(dst + i, vals[i], vals[i + 1], vals[i + 2], vals[i + 3]);
+    } else if constexpr (VPR % 4 == 0) {
 #pragma unroll
         for (int i = 0; i < VPR; i += 4) st256_cs(dst + i, vals[i], vals[i + 1], vals[i + 2], vals[i + 3]);
     } else if constexpr (VPR % 2 == 0) {
@@ -1161,7 +1198,7 @@ __device__ __forceinline__ void store_row(double *dst, const double (&vals)[VPR]
     }
 }
 
-template <int D, int M, int OPS, int A = 0>
+template <int D, int M, int OPS, int A = 0, bool KEEP = false>
 __device__ __forceinline__ void element_rows_store(const NumArgs &a, const ElemGeo<D> &g, const unsigned (&pos)[4])
 {
     constexpr int VPR = (D + 1) * n_outputs<OPS>() * M * M;
@@ -1170,7 +1207,7 @@ __device__ __forceinline__ void element_rows_store(const NumArgs &a, const ElemG
         general_all_rows<D>(a, g, K);
 #pragma unroll
         for (int al = 0; al <= D; ++al)
-            if (pos[al] != 0xffffffffu) store_row<D + 1>(a.kbuf + (int64_t)pos[al] * a.kstride, K[al]);
+            if (pos[al] != 0xffffffffu) store_row<D + 1, KEEP>(a.kbuf + (int64_t)pos[al] * a.kstride, K[al]);
         return;
     }
     if (pos[A] != 0xffffffffu) {
@@ -1188,7 +1225,7 @@ __device__ __forceinline__ void element_rows_store(const NumArgs &a, const ElemG
             for (int i = 0; i < VPR; ++i) dst[i] = vals[i];
         }
     }
-    if constexpr (A < D) element_rows_store<D, M, OPS, A + 1>(a, g, pos);
+    if constexpr (A < D) element_rows_store<D, M, OPS, A + 1, KEEP>(a, g, pos);
 }
 
 template <int D, int M, int OPS, int CORE, int MINB>
@@ -1256,7 +1293,8 @@ template <int D>
 __global__ void __launch_bounds__(EB_SIZE) k_eb_build(const typename IdxT<D>::type *__restrict__ me, int64_t e_lo,
                                                       int64_t ne, int32_t *__restrict__ verts,
                                                       int32_t *__restrict__ count, uint32_t *__restrict__ loc,
-                                                      unsigned long long *maxn)
+                                                      unsigned long long *maxn,
+                                                      const int32_t *__restrict__ elist = nullptr)
 {
     constexpr int NK = 4 * EB_SIZE;
     __shared__ int keys[NK];
@@ -1265,9 +1303,12 @@ __global__ void __launch_bounds__(EB_SIZE) k_eb_build(const typename IdxT<D>::ty
     const int t = threadIdx.x;
     const int64_t b = blockIdx.x, i = b * EB_SIZE + t;
     int v[D + 1];
-    if (i < ne) load_element<D>(me, e_lo + i, v);
+    // (elist: the batches cover a virtual element list; -1 entries are padding)
+    const int64_t e = i < ne ? (elist ? (int64_t)elist[i] : e_lo + i) : -1;
+    const bool have = e >= 0;
+    if (have) load_element<D>(me, e, v);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) keys[k * EB_SIZE + t] = (i < ne && k <= D) ? v[k < D + 1 ? k : 0] : INT_MAX;
+    for (int k = 0; k < 4; ++k) keys[k * EB_SIZE + t] = (have && k <= D) ? v[k < D + 1 ? k : 0] : INT_MAX;
     __syncthreads();
     // bitonic sort, NK/2 compare pairs per stage
     for (int kk = 2; kk <= NK; kk <<= 1)
@@ -1319,7 +1360,7 @@ __global__ void __launch_bounds__(EB_SIZE) k_eb_build(const typename IdxT<D>::ty
         count[b] = n <= EB_CAP ? n : -1;
         atomicMax(maxn, (unsigned long long)n);   // > EB_CAP: some batch takes the direct path
     }
-    if (i < ne && n <= EB_CAP) {
+    if (have && n <= EB_CAP) {
         unsigned l = 0;
 #pragma unroll
         for (int k = 0; k <= D; ++k) {
@@ -1365,7 +1406,7 @@ __device__ __forceinline__ void element_from_stage(const double *__restrict__ vr
 //   K[a][b] = G_a . Q_b + G_b . R_a + (a == b ? cd : co) ((a0s + a0_a) + a0_b)
 // ~210 fp64 instructions for the 16 entries instead of ~370 in reference
 // order.  Rows go to their incidence slots (pos) as in element_rows_store.
-template <int D, int CORE>
+template <int D, int CORE, bool KEEP = false>
 __device__ __forceinline__ bool stage_general_fast(const NumArgs &a, const double *__restrict__ vrec, unsigned lc,
                                                    double vol, const unsigned (&pos)[4])
 {
@@ -1449,7 +1490,7 @@ __device__ __forceinline__ bool stage_general_fast(const NumArgs &a, const doubl
     }
 #pragma unroll
     for (int al = 0; al <= D; ++al)
-        if (pos[al] != 0xffffffffu) store_row<D + 1>(a.kbuf + (int64_t)pos[al] * a.kstride, K[al]);
+        if (pos[al] != 0xffffffffu) store_row<D + 1, KEEP>(a.kbuf + (int64_t)pos[al] * a.kstride, K[al]);
     return deg;
 }
 
@@ -1467,7 +1508,11 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int D, int M, int OPS, int CORE, int MINB, bool FAST = false>
+// TILED: the batches walk a tile's virtual element list (a.elist: element of
+// each entry, -1 = padding; a.epos: tile-relative slots, ~0u = row outside
+// the tile) and the rows are stored with the default cache policy -- the
+// tile's fold reads them back from L2.
+template <int D, int M, int OPS, int CORE, int MINB, bool FAST = false, bool TILED = false>
 __global__ void __launch_bounds__(EB_SIZE, MINB) k_element_rows_pipe(NumArgs a)
 {
     extern __shared__ double dyn[];
@@ -1514,11 +1559,21 @@ __global__ void __launch_bounds__(EB_SIZE, MINB) k_element_rows_pipe(NumArgs a)
         lc = 0;
         vol = 0.0;
         if (bb < nb && i < a.ne) {
-            p = __ldcs(a.epos + i);
-            lc = __ldcs(a.eb_loc + i);
-            vol = __ldcs(a.vols + a.e_lo + i);
+            if constexpr (TILED) {
+                const int e = __ldcs(a.elist + i);
+                if (e >= 0) {
+                    p = __ldcs(a.epos + i);
+                    lc = __ldcs(a.eb_loc + i);
+                    vol = __ldg(a.vols + e);
+                }
+            } else {
+                p = __ldcs(a.epos + i);
+                lc = __ldcs(a.eb_loc + i);
+                vol = __ldcs(a.vols + a.e_lo + i);
+            }
         }
     };
+    auto elem_of = [&](int64_t i) -> int64_t { return TILED ? (int64_t)a.elist[i] : a.e_lo + i; };
     uint4 p;
     unsigned lc;
     double vol;
@@ -1543,16 +1598,16 @@ __global__ void __launch_bounds__(EB_SIZE, MINB) k_element_rows_pipe(NumArgs a)
         for (int kk = 0; kk <= D; ++kk) any |= pos[kk] != 0xffffffffu;
         if (i < a.ne && any) {
             if constexpr (FAST && OPS == OP_GENERAL) {
-                if (stage_general_fast<D, CORE>(a, recs + (size_t)(k & 1) * RS, lc, vol, pos))
-                    atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)(a.e_lo + i));
+                if (stage_general_fast<D, CORE, TILED>(a, recs + (size_t)(k & 1) * RS, lc, vol, pos))
+                    atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)elem_of(i));
             } else {
                 ElemRaw<D> x;
                 x.vol = vol;
                 element_from_stage<D, OPS>(recs + (size_t)(k & 1) * RS, lc, x);
                 ElemGeo<D> g;
                 if (element_compute<D, OPS, CORE>(x, g))
-                    atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)(a.e_lo + i));
-                element_rows_store<D, M, OPS>(a, g, pos);
+                    atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)elem_of(i));
+                element_rows_store<D, M, OPS, 0, TILED>(a, g, pos);
             }
         }
         p = pn;
@@ -1951,6 +2006,46 @@ int launch_twopass(const sa_plan *P, const NumArgs &a, int64_t nnodes, cudaStrea
     const bool pipe = GEN3 && a.eb_loc && a.gen_packed && a.eb_allfit;
     const bool fast = pipe && !a.exact;
     if constexpr (GEN3) {
+        if (pipe && P->tiled) {
+            // Tiled: per tile, the element pass over the tile's virtual
+            // elements, then the fold of its rows -- the tile's local rows
+            // (a reused ring buffer of at most tile_max_slots rows) never
+            // leave the L2.  Same per-element values, same fold order.
+            auto pk = fast ? k_element_rows_pipe<D, M, OPS, CORE, 2, true, true>
+                           : k_element_rows_pipe<D, M, OPS, CORE, 2, false, true>;
+            void (*fk)(NumArgs) = fast ? k_numeric_rowgather<D, M, OPS, CORE, 2, 1, true, false, true, true>
+                                       : k_numeric_rowgather<D, M, OPS, CORE, 2, 1, true, false, false, true>;
+            const size_t psm = 2 * (size_t)std::max(a.eb_maxn, 1) * EB_REC * sizeof(double) +
+                               3 * (EB_CAP + 1) * sizeof(int);
+            SA_CUDA_TRY(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+            int dev = 0, nsm = 148, occ = 0;
+            SA_CUDA_TRY(cudaGetDevice(&dev));
+            SA_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+            SA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pk, EB_SIZE, psm));
+            const size_t per_thread = (size_t)NOUT * (a.acc_stride | 1) * sizeof(double);
+            int block = 128;
+            while (per_thread * block > 100 * 1024 && block > 32) block /= 2;
+            const size_t smem = per_thread * block;
+            if (smem > 200 * 1024)
+                return set_error(SA_ERR_CAPACITY, "row accumulators need %zu B of shared memory per %d threads", smem,
+                                 block);
+            SA_CUDA_TRY(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            if (fast) SA_CUDA_TRY(cudaMemsetAsync(a.nflag, 0, sizeof(int), st));
+            NumArgs b = a;
+            for (int64_t t = 0; t < P->nt; ++t) {
+                b.eb_b0 = P->tile_v0[t] / EB_SIZE;
+                b.eb_b1 = P->tile_v0[t + 1] / EB_SIZE;
+                b.tw_p0 = P->tile_w0[t];
+                b.tw_p1 = P->tile_w0[t + 1];
+                const int64_t nb = b.eb_b1 - b.eb_b0;
+                if (nb)
+                    SA_LAUNCH(pk, (unsigned)std::min<int64_t>(nb, (int64_t)nsm * std::max(occ, 1)), EB_SIZE, psm, st, b);
+                const int64_t nr = 32 * (b.tw_p1 - b.tw_p0);
+                if (nr) SA_LAUNCH(fk, grid_for(nr, block), block, smem, st, b);
+            }
+            if (fast && nnodes) SA_LAUNCH((k_guard_fixup<D, OPS, CORE>), 148, 128, 0, st, a);
+            return SA_OK;
+        }
         if (pipe) {
             // (fast: 126 registers, 2 blocks of 256 per SM; batches of 256
             // elements read 7.7 instead of 9.5 GB -- C5 7.77 vs 7.90 ms)
@@ -2139,6 +2234,8 @@ static void free_all(std::initializer_list<void *> ps)
         if (p) cudaFreeAsync(p, 0);
 }
 
+#include "sa_tiles.cuh"
+
 // ===========================================================================
 // C ABI
 
@@ -2219,7 +2316,7 @@ int sa_plan_destroy(sa_plan *P)
     if (!P) return SA_OK;
     free_all({P->inc_ptr, P->inc, P->winc, P->wseg, P->colptr, P->cols, P->indptr, P->indices, P->counters,
               P->scan_tmp, P->epos, P->kbuf, P->tp_rank, P->eb_verts, P->eb_count, P->eb_loc, P->gd_flag_rows,
-              P->gd_nflag, P->heavy_rows});
+              P->gd_nflag, P->heavy_rows, P->tw_order, P->tw_vseg, P->tv_elem, P->tv_pos});
     delete P;
     return SA_OK;
 }
@@ -2271,16 +2368,18 @@ int sa_plan_info(const sa_plan *P, int64_t *nrows, int64_t *nnz, int64_t *max_ro
 int sa_plan_stats(const sa_plan *P, int64_t *out, int n)
 {
     if (!P || !out) return set_error(SA_ERR_ARG, "plan/out is NULL");
-    const int64_t nn = P->nnodes, nw = (nn + 31) / 32, ne = P->e_hi - P->e_lo, nb = (ne + EB_SIZE - 1) / EB_SIZE;
+    const int64_t nn = P->nnodes, nw = (nn + 31) / 32, ne = P->tiled ? P->nv : P->e_hi - P->e_lo,
+                  nb = (ne + EB_SIZE - 1) / EB_SIZE;
     // device bytes of the plan's symbolic structures (pattern, incidences,
     // warp records, two-pass slot map / row buffer / element batches)
     const int64_t bytes = 3 * (nn + 1) * 8 + P->n_inc * 8 + P->n_colnodes * 4 + (P->nrows + 1) * 8 + P->nnz * 4 +
                           P->n_winc * (int64_t)sizeof(IncRec) + (P->wseg ? (nw + 1) * 8 : 0) +
                           (P->epos ? ne * 16 : 0) + P->kbuf_elems * 8 + P->tp_nslots * 4 +
-                          (P->eb_loc ? ne * 4 + nb * (EB_CAP + 1) * 4 : 0);
-    const int64_t v[11] = {P->n_inc, P->max_deg, P->nnodes, P->nnz, P->n_winc, P->tp_nslots, P->eb_allfit ? 1 : 0,
-                           P->eb_maxn, bytes, P->light_deg, P->n_heavy};
-    for (int i = 0; i < n && i < 11; ++i) out[i] = v[i];
+                          (P->eb_loc ? ne * 4 + nb * (EB_CAP + 1) * 4 : 0) +
+                          (P->tiled ? P->nv * 20 + (2 * nw + 1) * 8 : 0);
+    const int64_t v[13] = {P->n_inc, P->max_deg, P->nnodes, P->nnz, P->n_winc, P->tp_nslots, P->eb_allfit ? 1 : 0,
+                           P->eb_maxn, bytes, P->light_deg, P->n_heavy, P->tiled ? P->nt : 0, P->tiled ? P->nv : 0};
+    for (int i = 0; i < n && i < 13; ++i) out[i] = v[i];
     return SA_OK;
 }
 
@@ -2311,7 +2410,7 @@ static bool want_twopass(int ops, int d, int m)
 // (built on first use, kept with the plan)
 static int ensure_twopass(sa_plan *P, int kstride, bool batches, cudaStream_t st)
 {
-    if (!P->epos) {
+    if (!P->epos && !P->tiled) {
         unsigned long long h[2] = {0xffffffffull, 0};
         unsigned long long *dr = nullptr;
         SA_CUDA_TRY(cudaMallocAsync((void **)&dr, 2 * sizeof(unsigned long long), st));
@@ -2326,25 +2425,35 @@ static int ensure_twopass(sa_plan *P, int kstride, bool batches, cudaStream_t st
         P->e_hi = P->n_inc ? (int64_t)h[1] + 1 : 0;
         const int64_t ne = P->e_hi - P->e_lo;
         const int64_t nn = P->nnodes, nw = (nn + 31) / 32;
-        if (!P->wseg) {   // warp-interleaved slot offsets (built with winc in 3D)
-            int64_t *span = nullptr;
-            SA_CUDA_TRY(cudaMallocAsync((void **)&span, (nw + 1) * sizeof(int64_t), st));
-            SA_CUDA_TRY(cudaMallocAsync((void **)&P->wseg, (nw + 1) * sizeof(int64_t), st));
-            if (nw) SA_LAUNCH(k_warp_span, grid_for(nw, 128), 128, 0, st, P->inc_ptr, nn, span);
-            SA_TRY(exclusive_scan_i64(span, P->wseg, nw, P->scan_tmp, st));
-            SA_CUDA_TRY(cudaFreeAsync(span, st));
+        int64_t *span = nullptr;
+        SA_CUDA_TRY(cudaMallocAsync((void **)&span, (nw + 1) * sizeof(int64_t), st));
+        if (nw) SA_LAUNCH(k_warp_span, grid_for(nw, 128), 128, 0, st, P->inc_ptr, nn, span);
+        // tiled schedule (3D general operator, coordinates known): the local
+        // rows of a tile stay in L2 (sa_tiles.cuh); SA_TUNE tile_kb = ring
+        // buffer budget, 0 = untiled
+        const int tile_kb = tune_int("tile_kb", 32 * 1024);
+        if (batches && P->mesh->d == 3 && !P->tile_tried && tile_kb > 0) {
+            const int rc = build_tiles(P, span, std::max<int64_t>((int64_t)tile_kb * 1024 / (kstride * 8), 32), st);
+            if (rc != SA_OK) { cudaFreeAsync(span, st); return rc; }
         }
-        SA_CUDA_TRY(cudaMemcpyAsync(&P->tp_nslots, P->wseg + nw, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
-        if (P->tp_nslots >= 0xffffffffLL)
-            return set_error(SA_ERR_CAPACITY, "two-pass numeric: %lld slots overflow 32-bit slot indices",
-                             (long long)P->tp_nslots);
-        SA_CUDA_TRY(cudaMallocAsync((void **)&P->epos, std::max<int64_t>(ne, 1) * sizeof(uint4), st));
-        SA_CUDA_TRY(cudaMemsetAsync(P->epos, 0xff, std::max<int64_t>(ne, 1) * sizeof(uint4), st));
-        SA_CUDA_TRY(cudaMallocAsync((void **)&P->tp_rank, std::max<int64_t>(P->tp_nslots, 1) * sizeof(unsigned), st));
-        if (nn)
-            SA_LAUNCH(k_tp_slots, grid_for(nn, 128), 128, 0, st, P->inc_ptr, P->inc, nn, P->wseg, (unsigned)P->e_lo,
-                      (unsigned *)P->epos, P->tp_rank);
+        if (!P->tiled) {
+            if (!P->wseg) {   // warp-interleaved slot offsets (built with winc in 3D)
+                SA_CUDA_TRY(cudaMallocAsync((void **)&P->wseg, (nw + 1) * sizeof(int64_t), st));
+                SA_TRY(exclusive_scan_i64(span, P->wseg, nw, P->scan_tmp, st));
+            }
+            SA_CUDA_TRY(cudaMemcpyAsync(&P->tp_nslots, P->wseg + nw, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            SA_CUDA_TRY(cudaStreamSynchronize(st));
+            if (P->tp_nslots >= 0xffffffffLL)
+                return set_error(SA_ERR_CAPACITY, "two-pass numeric: %lld slots overflow 32-bit slot indices",
+                                 (long long)P->tp_nslots);
+            SA_CUDA_TRY(cudaMallocAsync((void **)&P->epos, std::max<int64_t>(ne, 1) * sizeof(uint4), st));
+            SA_CUDA_TRY(cudaMemsetAsync(P->epos, 0xff, std::max<int64_t>(ne, 1) * sizeof(uint4), st));
+            SA_CUDA_TRY(cudaMallocAsync((void **)&P->tp_rank, std::max<int64_t>(P->tp_nslots, 1) * sizeof(unsigned), st));
+            if (nn)
+                SA_LAUNCH(k_tp_slots, grid_for(nn, 128), 128, 0, st, P->inc_ptr, P->inc, nn, P->wseg, (unsigned)P->e_lo,
+                          (unsigned *)P->epos, P->tp_rank);
+        }
+        SA_CUDA_TRY(cudaFreeAsync(span, st));
     }
     if (batches && !P->eb_loc && P->mesh->d == 3) {
         const int64_t ne = P->e_hi - P->e_lo, nb = (ne + EB_SIZE - 1) / EB_SIZE;
@@ -2368,7 +2477,7 @@ static int ensure_twopass(sa_plan *P, int kstride, bool batches, cudaStream_t st
         SA_CUDA_TRY(cudaMallocAsync((void **)&P->gd_flag_rows, std::max<int64_t>(P->nnodes, 1) * sizeof(uint32_t), st));
         SA_CUDA_TRY(cudaMallocAsync((void **)&P->gd_nflag, sizeof(int), st));
     }
-    const int64_t kelems = (int64_t)kstride * P->tp_nslots;
+    const int64_t kelems = (int64_t)kstride * (P->tiled ? P->tile_max_slots : P->tp_nslots);
     if (P->kbuf_elems < kelems) {
         if (P->kbuf) SA_CUDA_TRY(cudaFreeAsync(P->kbuf, st));
         P->kbuf = nullptr;
@@ -2471,6 +2580,14 @@ int sa_numeric(sa_plan *P, int ops, const sa_coeffs *cf, double *const *vals_dev
         a.epos = P->epos;
         a.e_lo = P->e_lo;
         a.ne = P->e_hi - P->e_lo;
+        if (P->tiled) {   // virtual element lists and tile-relative slots (sa_tiles.cuh)
+            a.epos = P->tv_pos;
+            a.elist = P->tv_elem;
+            a.e_lo = 0;
+            a.ne = P->nv;
+            a.tw_order = P->tw_order;
+            a.tw_vseg = P->tw_vseg;
+        }
         a.tp_rank = P->tp_rank;
         a.wseg = P->wseg;
         a.nflag = P->gd_nflag;
