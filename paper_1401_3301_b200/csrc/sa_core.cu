@@ -98,6 +98,13 @@ struct sa_plan {
     int64_t *tw_vseg = nullptr;     // (nw+1) virtual slot offset of each sorted position
     int32_t *tv_elem = nullptr;     // (nv) element of each virtual element, -1 = padding
     uint4 *tv_pos = nullptr;        // (nv) tile-relative slots of its 4 local rows, ~0u = row outside the tile
+    // tiles run round-robin on tile_ns internal streams (each with its own
+    // ring buffer), so the element pass of one tile overlaps the fold of another
+    int64_t *tile_dev = nullptr;    // 3 x (nt+1): batch, sorted-warp and fold-chunk prefix of each tile (fused kernel)
+    unsigned *tile_sync = nullptr;  // 2 x nt completion counters (fused kernel)
+    int tile_ns = 0;
+    cudaStream_t tile_st[8] = {};
+    cudaEvent_t tile_ev[9] = {};
 };
 
 // numeric-phase arguments (shared by the per-dimension translation units)
@@ -149,6 +156,14 @@ struct NumArgs {
     const uint32_t *tw_order;
     const int64_t *tw_vseg;
     int64_t tw_p0, tw_p1;
+    // fused tiled kernel: per tile its batch range, sorted-warp range and fold
+    // chunk range (prefix arrays of nt + 1), completion counters
+    // (element batches done [nt], fold chunks done [nt]), ring slots per tile
+    const int64_t *tile_b, *tile_p, *tile_fc;
+    unsigned *tile_sync;
+    int nt;
+    int64_t ring_slots;
+    int dbg;   // timing experiments only (SA_TUNE tile_dbg): 1 = no folds, 2 = no element pass
 };
 
 namespace {
@@ -1618,6 +1633,265 @@ __global__ void __launch_bounds__(EB_SIZE, MINB) k_element_rows_pipe(NumArgs a)
     cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------------------------
+// Fused tiled two-pass (3D general operator): ONE persistent kernel runs the
+// element pass and the fold of every tile.  Batch g of the global batch list
+// (tiles in order) belongs to CTA g mod G, so the three-stage cp.async
+// pipeline of k_element_rows_pipe runs across tile boundaries without
+// draining; when a CTA's next batch belongs to tile p it first folds its share
+// (chunks of 8 sorted warps, chunk h of the global chunk list to CTA h mod G)
+// of the tiles up to p - 2, whose local rows sit in a ring of TILE_RING tile
+// buffers that stays in L2.  Tiles hand over through two counters per tile
+// (element batches done, fold chunks done): release = __threadfence + atomic
+// after a CTA barrier, acquire = ld.acquire.gpu spin by one thread + barrier;
+// the ring is read with ld.global.cg (L2: its addresses are rewritten every
+// TILE_RING tiles, an L1 line could be stale).  Every wait refers to work of
+// earlier tiles that its owner reaches earlier in its own program order, and
+// all CTAs are resident (grid = occupancy x SMs), so the waits cannot cycle;
+// they are bounded anyway (counters[7] = timeout -> SA_ERR_CUDA).  Same
+// element values and fold order as the two-kernel path: bitwise identical.
+constexpr int TILE_RING = 3;
+constexpr int TILE_FCH = EB_SIZE / 32;   // sorted warps per fold chunk
+
+__device__ __forceinline__ void ld256_cg(const double *p, double &a, double &b, double &c, double &d)
+{
+    asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p) : "memory");
+}
+
+template <int CORE, bool FAST>
+__global__ void __launch_bounds__(EB_SIZE, 2) k_tiled_fused(NumArgs a)
+{
+    constexpr int D = 3;
+    constexpr int OPS = OP_GENERAL;
+    extern __shared__ double dyn[];
+    double *recs = dyn;                                                 // [2][maxn][EB_REC]
+    int *svs = (int *)(dyn + 2 * (size_t)a.eb_maxn * EB_REC);           // [3][EB_CAP + 1] (+ count)
+    double *facc = (double *)(svs + 3 * (EB_CAP + 1));                  // fold accumulators [8 warps][32][acc_stride | 1]
+    const int t = threadIdx.x, lane = t & 31, wp = t >> 5;
+    const int64_t nb = a.eb_b1;   // all batches of all tiles
+    const int64_t G = gridDim.x;
+    const int RS = a.eb_maxn * EB_REC;
+    unsigned long long *abort_flag = (unsigned long long *)(a.counters + 7);
+
+    auto wait_count = [&](const unsigned *ctr, unsigned target) {
+        if (t == 0) {
+            unsigned v;
+            for (int spins = 0;; ++spins) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+                if (v >= target) break;
+                if (*(volatile unsigned long long *)abort_flag) break;
+                if (spins > (1 << 21)) { atomicExch(abort_flag, 1ull); break; }
+                __nanosleep(64);
+            }
+        }
+        __syncthreads();
+    };
+    auto signal = [&](unsigned *ctr) {
+        __threadfence();
+        __syncthreads();
+        if (t == 0) atomicAdd(ctr, 1u);
+    };
+
+    // ---- fold of chunk j of tile q (the PRE/TILED path of k_numeric_rowgather, M = 1)
+    auto fold_chunk = [&](int q, int64_t j) {
+        const unsigned full = 0xffffffffu;
+        const int64_t p0 = a.tile_p[q], p1 = a.tile_p[q + 1];
+        const int64_t tpos = p0 + TILE_FCH * j + wp;
+        const int64_t nl = tpos < p1 ? (int64_t)a.tw_order[tpos] * 32 + lane : a.nnodes;
+        const bool in_range = nl < a.nnodes;
+        const int64_t c0 = in_range ? a.colptr[nl] : 0;
+        const int deg_row = in_range ? (int)(a.colptr[nl + 1] - c0) : -1;
+        const bool active = in_range && deg_row <= a.light_deg;
+        const int deg = active ? deg_row : -1;
+        const int64_t row_base = active ? a.indptr[nl] : 0;
+        const int n_inc = active ? (int)(a.inc_ptr[nl + 1] - a.inc_ptr[nl]) : 0;
+        const int d0 = __shfl_sync(full, deg, 0);
+        const bool uniform = __all_sync(full, deg == d0) && d0 > 0;
+        int dmax = deg;
+#pragma unroll
+        for (int sh = 16; sh > 0; sh >>= 1) dmax = max(dmax, __shfl_xor_sync(full, dmax, sh));
+        const int S = uniform ? d0 : (max(dmax, 0) | 1);
+        double *wacc = facc + (size_t)wp * 32 * (a.acc_stride | 1) + lane * S;
+        double rbound = 0.0;
+        int nz = 0;
+        if (active) {
+            for (int k = 0; k < deg; ++k) wacc[k] = 0.0;
+            const int64_t vs = a.tw_vseg[tpos];
+            const unsigned *rk = a.tp_rank + vs + lane;
+            const double *kb = a.kbuf + ((int64_t)(q % TILE_RING) * a.ring_slots + (vs - a.tw_vseg[p0]) + lane) * 4;
+            auto accum = [&](const double(&v)[4], unsigned ranks) {
+                if constexpr (FAST) rbound += fabs(v[0]) + fabs(v[1]) + fabs(v[2]) + fabs(v[3]);
+#pragma unroll
+                for (int b = 0; b < 4; ++b) wacc[(ranks >> (8 * b)) & 0xff] += v[b];
+            };
+            constexpr int U = 4;
+            int k = 0;
+            for (; k + U <= n_inc; k += U) {
+                unsigned r[U];
+                double v[U][4];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    r[u] = __ldcs(rk + 32 * (k + u));
+                    ld256_cg(kb + 128 * (int64_t)(k + u), v[u][0], v[u][1], v[u][2], v[u][3]);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) accum(v[u], r[u]);
+            }
+            for (; k < n_inc; ++k) {
+                double v[4];
+                const unsigned r = __ldcs(rk + 32 * k);
+                ld256_cg(kb + 128 * (int64_t)k, v[0], v[1], v[2], v[3]);
+                accum(v, r);
+            }
+        }
+        __syncwarp();
+        if constexpr (FAST) {
+            if (active) {
+                bool flag = false;
+                const double thr = SA_GUARD_TAU * rbound;
+                for (int k = 0; k < deg; ++k) flag |= fabs(wacc[k]) <= thr;
+                if (flag) a.flag_rows[atomicAdd(a.nflag, 1)] = (uint32_t)nl;
+            }
+        }
+        if (uniform) {
+            const int64_t base = __shfl_sync(full, row_base, 0);
+            const double *plane = wacc - lane * S;
+            for (int i = lane; i < 32 * S; i += 32) {
+                const double val = plane[i];
+                __stcs(a.vals[0] + base + i, val);
+                if constexpr (!FAST) nz += (val == 0.0);
+            }
+        } else if (active) {
+            for (int k = 0; k < deg; ++k) {
+                const double val = wacc[k];
+                __stcs(a.vals[0] + row_base + k, val);
+                if constexpr (!FAST) nz += (val == 0.0);
+            }
+        }
+        if constexpr (!FAST) {
+#pragma unroll
+            for (int sh = 16; sh > 0; sh >>= 1) nz += __shfl_xor_sync(full, nz, sh);
+            if (lane == 0 && nz) atomicAdd((unsigned long long *)a.counters, (unsigned long long)nz);
+        }
+    };
+    int fnext = 0;   // first tile whose fold chunks this CTA has not done yet
+    auto do_folds = [&](int upto) {
+        if (a.dbg == 1) return;
+        for (; fnext < upto; ++fnext) {
+            const int64_t c0 = a.tile_fc[fnext], c1 = a.tile_fc[fnext + 1];
+            int64_t h = c0 + (((int64_t)blockIdx.x - c0 % G) + G) % G;
+            if (h >= c1) continue;
+            if (a.dbg != 2) wait_count(a.tile_sync + fnext, (unsigned)(a.tile_b[fnext + 1] - a.tile_b[fnext]));
+            for (; h < c1; h += G) {
+                fold_chunk(fnext, h - c0);
+                signal(a.tile_sync + a.nt + fnext);
+            }
+        }
+    };
+
+    // ---- element pass (k_element_rows_pipe over the global batch list)
+    auto issue_list = [&](int64_t bb, int stage) {
+        if (bb >= nb) return;
+        int *sv = svs + stage * (EB_CAP + 1);
+        const int32_t *vl = a.eb_verts + bb * EB_CAP;
+        for (int s = t; s < EB_CAP; s += EB_SIZE) cp_async4(sv + s, vl + s);
+        if (t == 0) cp_async4(sv + EB_CAP, a.eb_count + bb);
+    };
+    auto issue_recs = [&](int64_t bb, int lstage, int rstage) {
+        if (bb >= nb) return;
+        const int *sv = svs + lstage * (EB_CAP + 1);
+        double *rec = recs + (size_t)rstage * RS;
+        const int n = sv[EB_CAP];
+        for (int c = t; c < n * 10; c += EB_SIZE) {
+            const int s = c / 10, h = c - 10 * s;
+            const int64_t vv = sv[s];
+            const double *src = h < 2 ? (const double *)a.qv + vv * 4 + 2 * h : a.gen_packed + vv * 16 + 2 * (h - 2);
+            cp_async16(rec + s * EB_REC + 2 * h, src);
+        }
+    };
+    auto own = [&](int64_t bb, uint4 &p, unsigned &lc, double &vol) {
+        const int64_t i = bb * EB_SIZE + t;
+        p = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+        lc = 0;
+        vol = 0.0;
+        if (bb < nb) {
+            const int e = __ldcs(a.elist + i);
+            if (e >= 0) {
+                p = __ldcs(a.epos + i);
+                lc = __ldcs(a.eb_loc + i);
+                vol = __ldg(a.vols + e);
+            }
+        }
+    };
+    const int64_t b0 = blockIdx.x;
+    if (b0 < nb && a.dbg != 2) {
+        issue_list(b0, 0);
+        cp_async_commit();
+        issue_list(b0 + G, 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        issue_recs(b0, 0, 0);
+        cp_async_commit();
+        uint4 p;
+        unsigned lc;
+        double vol;
+        own(b0, p, lc, vol);
+        int tile = -1;
+        unsigned roff = 0;
+        for (int64_t k = 0;; ++k) {
+            const int64_t b = b0 + k * G;
+            if (b >= nb) break;
+            issue_list(b + 2 * G, (int)((k + 2) % 3));
+            cp_async_commit();
+            cp_async_wait<1>();   // records of batch k and the list of batch k+1 have landed
+            __syncthreads();
+            issue_recs(b + G, (int)((k + 1) % 3), (int)((k + 1) & 1));
+            cp_async_commit();
+            uint4 pn;
+            unsigned lcn;
+            double voln;
+            own(b + G, pn, lcn, voln);
+            if (tile < 0 || b >= a.tile_b[tile + 1]) {   // first batch of a new tile (uniform over the CTA)
+                do ++tile; while (b >= a.tile_b[tile + 1]);
+                do_folds(tile - 1);
+                if (tile >= TILE_RING && a.dbg != 1)   // the ring buffer of this tile was read by the folds of tile - TILE_RING
+                    wait_count(a.tile_sync + a.nt + tile - TILE_RING,
+                               (unsigned)(a.tile_fc[tile - TILE_RING + 1] - a.tile_fc[tile - TILE_RING]));
+                roff = (unsigned)((tile % TILE_RING) * a.ring_slots);
+            }
+            const int64_t i = b * EB_SIZE + t;
+            unsigned pos[4] = {p.x, p.y, p.z, p.w};
+            bool any = false;
+#pragma unroll
+            for (int kk = 0; kk <= D; ++kk) {
+                any |= pos[kk] != 0xffffffffu;
+                if (pos[kk] != 0xffffffffu) pos[kk] += roff;
+            }
+            if (any) {
+                if constexpr (FAST) {
+                    if (stage_general_fast<D, CORE, true>(a, recs + (size_t)(k & 1) * RS, lc, vol, pos))
+                        atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)a.elist[i]);
+                } else {
+                    ElemRaw<D> x;
+                    x.vol = vol;
+                    element_from_stage<D, OPS>(recs + (size_t)(k & 1) * RS, lc, x);
+                    ElemGeo<D> g;
+                    if (element_compute<D, OPS, CORE>(x, g))
+                        atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)a.elist[i]);
+                    element_rows_store<D, 1, OPS, 0, true>(a, g, pos);
+                }
+            }
+            p = pn;
+            lc = lcn;
+            vol = voln;
+            signal(a.tile_sync + tile);   // (its barrier also frees stage k & 1 for the records of batch k+2)
+        }
+        cp_async_wait<0>();
+    }
+    do_folds(a.nt);
+}
+
 // element range of the block's incidences: out[0] = min e, out[1] = max e
 __global__ void k_inc_erange(const uint2 *__restrict__ inc, int64_t n, unsigned long long *out)
 {
@@ -2032,16 +2306,48 @@ int launch_twopass(const sa_plan *P, const NumArgs &a, int64_t nnodes, cudaStrea
             SA_CUDA_TRY(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             if (fast) SA_CUDA_TRY(cudaMemsetAsync(a.nflag, 0, sizeof(int), st));
             NumArgs b = a;
+            if (tune_int("tile_fused", 1) != 0 && block == 128) {
+                // one persistent kernel for every tile (k_tiled_fused)
+                auto uk = fast ? k_tiled_fused<CORE, true> : k_tiled_fused<CORE, false>;
+                const size_t usm = psm + (size_t)TILE_FCH * 32 * (a.acc_stride | 1) * sizeof(double);
+                SA_CUDA_TRY(cudaFuncSetAttribute(uk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm));
+                int uocc = 0;
+                SA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&uocc, uk, EB_SIZE, usm));
+                if (uocc >= 1) {
+                    SA_CUDA_TRY(cudaMemsetAsync(P->tile_sync, 0, 2 * P->nt * sizeof(unsigned), st));
+                    b.eb_b0 = 0;
+                    b.eb_b1 = P->nv / EB_SIZE;
+                    b.tile_b = P->tile_dev;
+                    b.tile_p = P->tile_dev + (P->nt + 1);
+                    b.tile_fc = P->tile_dev + 2 * (P->nt + 1);
+                    b.tile_sync = P->tile_sync;
+                    b.nt = (int)P->nt;
+                    b.ring_slots = P->tile_max_slots;
+                    b.dbg = tune_int("tile_dbg", 0);
+                    SA_LAUNCH(uk, (unsigned)(nsm * uocc), EB_SIZE, usm, st, b);
+                    if (fast && nnodes) SA_LAUNCH((k_guard_fixup<D, OPS, CORE>), 148, 128, 0, st, a);
+                    return SA_OK;
+                }
+            }
+            const int ns = P->tile_ns;
+            SA_CUDA_TRY(cudaEventRecord(P->tile_ev[ns], st));
+            for (int s = 0; s < ns; ++s) SA_CUDA_TRY(cudaStreamWaitEvent(P->tile_st[s], P->tile_ev[ns], 0));
             for (int64_t t = 0; t < P->nt; ++t) {
+                cudaStream_t ts = P->tile_st[t % ns];
+                b.kbuf = a.kbuf + (t % ns) * P->tile_max_slots * a.kstride;
                 b.eb_b0 = P->tile_v0[t] / EB_SIZE;
                 b.eb_b1 = P->tile_v0[t + 1] / EB_SIZE;
                 b.tw_p0 = P->tile_w0[t];
                 b.tw_p1 = P->tile_w0[t + 1];
                 const int64_t nb = b.eb_b1 - b.eb_b0;
                 if (nb)
-                    SA_LAUNCH(pk, (unsigned)std::min<int64_t>(nb, (int64_t)nsm * std::max(occ, 1)), EB_SIZE, psm, st, b);
+                    SA_LAUNCH(pk, (unsigned)std::min<int64_t>(nb, (int64_t)nsm * std::max(occ, 1)), EB_SIZE, psm, ts, b);
                 const int64_t nr = 32 * (b.tw_p1 - b.tw_p0);
-                if (nr) SA_LAUNCH(fk, grid_for(nr, block), block, smem, st, b);
+                if (nr) SA_LAUNCH(fk, grid_for(nr, block), block, smem, ts, b);
+            }
+            for (int s = 0; s < ns; ++s) {
+                SA_CUDA_TRY(cudaEventRecord(P->tile_ev[s], P->tile_st[s]));
+                SA_CUDA_TRY(cudaStreamWaitEvent(st, P->tile_ev[s], 0));
             }
             if (fast && nnodes) SA_LAUNCH((k_guard_fixup<D, OPS, CORE>), 148, 128, 0, st, a);
             return SA_OK;
@@ -2314,9 +2620,15 @@ int sa_mesh_destroy(sa_mesh *M)
 int sa_plan_destroy(sa_plan *P)
 {
     if (!P) return SA_OK;
+    for (int s = 0; s < P->tile_ns; ++s) {
+        cudaStreamSynchronize(P->tile_st[s]);
+        cudaStreamDestroy(P->tile_st[s]);
+        cudaEventDestroy(P->tile_ev[s]);
+    }
+    if (P->tile_ns) cudaEventDestroy(P->tile_ev[P->tile_ns]);
     free_all({P->inc_ptr, P->inc, P->winc, P->wseg, P->colptr, P->cols, P->indptr, P->indices, P->counters,
               P->scan_tmp, P->epos, P->kbuf, P->tp_rank, P->eb_verts, P->eb_count, P->eb_loc, P->gd_flag_rows,
-              P->gd_nflag, P->heavy_rows, P->tw_order, P->tw_vseg, P->tv_elem, P->tv_pos});
+              P->gd_nflag, P->heavy_rows, P->tw_order, P->tw_vseg, P->tv_elem, P->tv_pos, P->tile_dev, P->tile_sync});
     delete P;
     return SA_OK;
 }
@@ -2477,7 +2789,16 @@ static int ensure_twopass(sa_plan *P, int kstride, bool batches, cudaStream_t st
         SA_CUDA_TRY(cudaMallocAsync((void **)&P->gd_flag_rows, std::max<int64_t>(P->nnodes, 1) * sizeof(uint32_t), st));
         SA_CUDA_TRY(cudaMallocAsync((void **)&P->gd_nflag, sizeof(int), st));
     }
-    const int64_t kelems = (int64_t)kstride * (P->tiled ? P->tile_max_slots : P->tp_nslots);
+    if (P->tiled && !P->tile_ns) {
+        const int ns = std::min(8, std::max(1, tune_int("tile_streams", 3)));
+        for (int s = 0; s < ns; ++s) {
+            SA_CUDA_TRY(cudaStreamCreateWithFlags(&P->tile_st[s], cudaStreamNonBlocking));
+            SA_CUDA_TRY(cudaEventCreateWithFlags(&P->tile_ev[s], cudaEventDisableTiming));
+        }
+        SA_CUDA_TRY(cudaEventCreateWithFlags(&P->tile_ev[ns], cudaEventDisableTiming));
+        P->tile_ns = ns;
+    }
+    const int64_t kelems = (int64_t)kstride * (P->tiled ? std::max(P->tile_ns, TILE_RING) * P->tile_max_slots : P->tp_nslots);
     if (P->kbuf_elems < kelems) {
         if (P->kbuf) SA_CUDA_TRY(cudaFreeAsync(P->kbuf, st));
         P->kbuf = nullptr;

@@ -19,12 +19,11 @@
 // and runs of whole bricks are packed greedily up to the slot budget (a brick
 // above the budget is split).  Meshes whose numbering has no locality give
 // tiles with large halos; the caller keeps the untiled path when the
-// recomputation factor exceeds TILE_MAX_FACTOR.
+// recomputation factor exceeds 1.6.
 #pragma once
 
 namespace {
 
-constexpr double TILE_MAX_FACTOR = 1.6;
 
 __device__ __forceinline__ unsigned long long ordered_bits(double x)
 {
@@ -374,7 +373,8 @@ int build_tiles(sa_plan *P, const int64_t *span, int64_t slot_budget, cudaStream
         v0[t + 1] = v0[t] + (c + EB_SIZE - 1) / EB_SIZE * EB_SIZE;
     }
     const int64_t nv = v0[nt];
-    if ((double)hpre[nt] > TILE_MAX_FACTOR * (double)ne || nv >= 0x7fffffffLL) return SA_OK;   // halos too large
+    // halos too large (SA_TUNE tile_maxf, percent: tests force tiny tiles)
+    if ((double)hpre[nt] > 0.01 * tune_int("tile_maxf", 160) * (double)ne || nv >= 0x7fffffffLL) return SA_OK;
     {
         std::vector<int64_t> pre(nw + 1, 0);
         for (int64_t p = 0; p < nw; ++p) pre[p + 1] = pre[p] + hspan[p];
@@ -420,6 +420,20 @@ int build_tiles(sa_plan *P, const int64_t *span, int64_t slot_budget, cudaStream
     }
     P->eb_maxn = (int)hmx;
     P->eb_allfit = true;
+    {   // per-tile prefix arrays of the fused kernel: batches, sorted warps, fold chunks
+        std::vector<int64_t> hd(3 * (nt + 1));
+        for (int t = 0; t <= nt; ++t) {
+            hd[t] = v0[t] / EB_SIZE;
+            hd[(nt + 1) + t] = w0[t];
+        }
+        hd[2 * (nt + 1)] = 0;
+        for (int t = 0; t < nt; ++t)
+            hd[2 * (nt + 1) + t + 1] = hd[2 * (nt + 1) + t] + (w0[t + 1] - w0[t] + TILE_FCH - 1) / TILE_FCH;
+        SA_CUDA_TRY(cudaMallocAsync((void **)&P->tile_dev, hd.size() * sizeof(int64_t), st));
+        SA_CUDA_TRY(cudaMallocAsync((void **)&P->tile_sync, 2 * (size_t)nt * sizeof(unsigned), st));
+        SA_CUDA_TRY(cudaMemcpyAsync(P->tile_dev, hd.data(), hd.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        SA_CUDA_TRY(cudaStreamSynchronize(st));
+    }
     // keep: order, vseg (taken out of the temporaries)
     for (void *&p : tmp.ps)
         if (p == (void *)order || p == (void *)vseg) p = nullptr;

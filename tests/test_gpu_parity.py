@@ -734,9 +734,10 @@ def _plan_general(mesh, k):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("fused", [1, 0])
 @pytest.mark.parametrize("exact", [True, False])
 @pytest.mark.parametrize("tile_kb", [8, 64, 1024])
-def test_general_tiled_bitwise_untiled(cuda_ok, tile_kb, exact, monkeypatch):
+def test_general_tiled_bitwise_untiled(cuda_ok, tile_kb, exact, fused, monkeypatch):
     # tiled two-pass (sa_tiles.cuh): rows grouped into L2-sized spatial tiles,
     # each tile's elements (halo included) computed into a reused ring
     # buffer and folded at once.  Same element values, same fold order:
@@ -748,7 +749,9 @@ def test_general_tiled_bitwise_untiled(cuda_ok, tile_kb, exact, monkeypatch):
     tune(monkeypatch, tile_kb=0)
     st0, ip0, ix0, v0, z0 = _plan_general(mesh, k)
     assert st0["tiles"] == 0
-    tune(monkeypatch, tile_kb=tile_kb)
+    # fused: one persistent kernel for all tiles (default); 0: one element-pass
+    # and one fold launch per tile, round-robin on internal streams
+    tune(monkeypatch, tile_kb=tile_kb, tile_maxf=1000, tile_fused=fused)
     st, ip, ix, v, z = _plan_general(mesh, k)
     assert st["tiles"] >= 2 and st["tile_elements"] >= mesh.me.shape[1]
     assert np.array_equal(ip, ip0) and np.array_equal(ix, ix0) and z == z0
@@ -765,7 +768,7 @@ def test_general_tiled_guard_hub_and_blocks(cuda_ok, monkeypatch):
     # the plan keeps the untiled path)
     from oracle import oracle as O
 
-    tune(monkeypatch, tile_kb=64)
+    tune(monkeypatch, tile_kb=64, tile_maxf=300)
     q, me = P.hypercube_arrays(3, 12)
     mesh = P.Mesh(q, me, O.volumes(q, me))
     nq = q.shape[1]
