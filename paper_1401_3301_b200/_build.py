@@ -17,7 +17,7 @@ LIBDIR = os.path.join(HERE, "_lib")
 LIBNAME = "libsimplex_asm_b200.so"
 LIB_PATH = os.path.join(LIBDIR, LIBNAME)
 SOURCES = ["sa_abi.cu", "sa_d1.cu", "sa_d2.cu", "sa_d3.cu", "sa_scan.cu", "sa_meshgen.cu"]
-HEADERS = ["sa_common.cuh", "sa_geometry.cuh", "sa_core.cu", "sa_pk.cuh", "sa_tiles.cuh"]
+HEADERS = ["sa_common.cuh", "sa_geometry.cuh", "sa_core.cu", "sa_pk.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

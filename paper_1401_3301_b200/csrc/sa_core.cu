@@ -13,7 +13,6 @@
 // No atomics touch values: the output is deterministic by construction.
 #include <algorithm>
 #include <climits>
-#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -88,23 +87,6 @@ struct sa_plan {
     // heavy rows (degree above the light cap): assembled by k_heavy_rows
     int64_t light_deg = 0, n_heavy = 0;
     uint32_t *heavy_rows = nullptr;
-    // tiled two-pass (sa_tiles.cuh): rows grouped into spatial tiles whose
-    // local rows fit the L2; per tile the touching elements (virtual element
-    // list, batch-aligned) and tile-relative slots into a reused ring buffer
-    bool tiled = false, tile_tried = false;
-    int64_t nt = 0, nv = 0, tile_max_slots = 0;
-    std::vector<int64_t> tile_w0, tile_v0;   // (nt+1) sorted-warp / virtual-element range of each tile
-    uint32_t *tw_order = nullptr;   // (nw) the warp (of 32 node rows) at each sorted position
-    int64_t *tw_vseg = nullptr;     // (nw+1) virtual slot offset of each sorted position
-    int32_t *tv_elem = nullptr;     // (nv) element of each virtual element, -1 = padding
-    uint4 *tv_pos = nullptr;        // (nv) tile-relative slots of its 4 local rows, ~0u = row outside the tile
-    // tiles run round-robin on tile_ns internal streams (each with its own
-    // ring buffer), so the element pass of one tile overlaps the fold of another
-    int64_t *tile_dev = nullptr;    // 3 x (nt+1): batch, sorted-warp and fold-chunk prefix of each tile (fused kernel)
-    unsigned *tile_sync = nullptr;  // 2 x nt completion counters (fused kernel)
-    int tile_ns = 0;
-    cudaStream_t tile_st[8] = {};
-    cudaEvent_t tile_ev[9] = {};
 };
 
 // numeric-phase arguments (shared by the per-dimension translation units)
@@ -150,20 +132,6 @@ struct NumArgs {
     int light_deg;       // rows with more columns are heavy (k_heavy_rows), skipped by the row kernels
     const uint32_t *heavy_rows;
     int64_t n_heavy;
-    // tiled two-pass: virtual element list (element pass), sorted warp
-    // positions [tw_p0, tw_p1) of the tile (fold)
-    const int32_t *elist;
-    const uint32_t *tw_order;
-    const int64_t *tw_vseg;
-    int64_t tw_p0, tw_p1;
-    // fused tiled kernel: per tile its batch range, sorted-warp range and fold
-    // chunk range (prefix arrays of nt + 1), completion counters
-    // (element batches done [nt], fold chunks done [nt]), ring slots per tile
-    const int64_t *tile_b, *tile_p, *tile_fc;
-    unsigned *tile_sync;
-    int nt;
-    int64_t ring_slots;
-    int dbg;   // timing experiments only (SA_TUNE tile_dbg): 1 = no folds, 2 = no element pass
 };
 
 namespace {
@@ -922,11 +890,9 @@ __device__ __forceinline__ void krow_runtime(const NumArgs &a, const ElemGeo<D> 
 // accumulators indexed by the 8-bit column ranks stored with each incidence.
 // Used when a node has more than 31 incidences or the block kernel's shared
 // memory does not fit.
-template <int D, int M, int OPS, int CORE, int ILP, int MINB, bool PRE = false, bool LEAN = false, bool GUARD = false,
-          bool TILED = false>
+template <int D, int M, int OPS, int CORE, int ILP, int MINB, bool PRE = false, bool LEAN = false, bool GUARD = false>
 __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
 {
-    static_assert(!TILED || PRE, "tiles serve the two-pass fold only");
     // LEAN: a constant mass weight, known at compile time (the local copy is
     // scalar-replaced; w == nullptr folds the weight loads away)
     NumArgs a = a_in;
@@ -934,14 +900,7 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
     constexpr int NOUT = n_outputs<OPS>();
     extern __shared__ double smem_acc[];
     const int tid = threadIdx.x, lane = tid & 31;
-    // TILED: the block's warps are sorted positions tw_p0 + ... of the tile;
-    // position p holds the 32 node rows of warp tw_order[p]
-    int64_t nl = blockIdx.x * (int64_t)blockDim.x + tid;
-    int64_t tpos = 0;
-    if constexpr (TILED) {
-        tpos = a.tw_p0 + (nl >> 5);
-        nl = tpos < a.tw_p1 ? (int64_t)a.tw_order[tpos] * 32 + lane : a.nnodes;
-    }
+    const int64_t nl = blockIdx.x * (int64_t)blockDim.x + tid;
     // Accumulators: per warp and output a plane of 32 lane rows of S doubles;
     // lane j's dof row l, column k at wacc[o*32*S + j*S + l*M*deg + k].  When
     // the warp's rows all have degree d0, S = M*M*d0 and the plane IS the
@@ -1038,16 +997,10 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
             // the warp at wseg + 32 k + j, so each warp load is one contiguous
             // run); ranks and rows are independent loads -- no gather chain,
             // U incidences in flight
-            // (TILED: ranks in virtual slot order, rows in the tile's ring
-            // buffer at tile-relative slots -- L2 hits, default policy)
-            const int64_t sb = TILED ? a.tw_vseg[tpos] + lane : a.wseg[nl >> 5] + lane;
-            const int64_t kofs = TILED ? a.tw_vseg[a.tw_p0] : 0;
+            const int64_t sb = a.wseg[nl >> 5] + lane;
             auto loadk = [&](int64_t slot, double(&v)[VPR]) {
-                const double *src = a.kbuf + (slot - kofs) * a.kstride;
-                if constexpr (VPR % 4 == 0 && TILED) {
-#pragma unroll
-                    for (int i = 0; i < VPR; i += 4) ldg256(src + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
-                } else if constexpr (VPR % 4 == 0) {
+                const double *src = a.kbuf + slot * a.kstride;
+                if constexpr (VPR % 4 == 0) {
 #pragma unroll
                     for (int i = 0; i < VPR; i += 4) ldg256_cs(src + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
                 } else if constexpr (VPR % 2 == 0) {
@@ -1145,8 +1098,7 @@ __global__ void __launch_bounds__(128, MINB) k_numeric_rowgather(NumArgs a_in)
 #pragma unroll
             for (int o = 0; o < NOUT; ++o) {
                 const double val = plane[o * 32 * S + i];
-                if constexpr (TILED) __stcs(a.vals[o] + base + i, val);   // streamed: keep the ring in L2
-                else a.vals[o][base + i] = val;
+                a.vals[o][base + i] = val;
                 if constexpr (!GUARD) nz[o] += (val == 0.0);
             }
         }
@@ -1194,14 +1146,10 @@ __device__ __forceinline__ void st256_cs(double *p, double a, double b, double c
     asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
 
-// KEEP: default cache policy (tiled two-pass: the fold reads the row back from L2)
-template <int VPR, bool KEEP = false>
+template <int VPR>
 __device__ __forceinline__ void store_row(double *dst, const double (&vals)[VPR])
 {
-    if constexpr (VPR % 4 == 0 && KEEP) {
-#pragma unroll
-        for (int i = 0; i < VPR; i += 4) st256(dst + i, vals[i], vals[i + 1], vals[i + 2], vals[i + 3]);
-    } else if constexpr (VPR % 4 == 0) {
+    if constexpr (VPR % 4 == 0) {
 #pragma unroll
         for (int i = 0; i < VPR; i += 4) st256_cs(dst + i, vals[i], vals[i + 1], vals[i + 2], vals[i + 3]);
     } else if constexpr (VPR % 2 == 0) {
@@ -1213,7 +1161,7 @@ __device__ __forceinline__ void store_row(double *dst, const double (&vals)[VPR]
     }
 }
 
-template <int D, int M, int OPS, int A = 0, bool KEEP = false>
+template <int D, int M, int OPS, int A = 0>
 __device__ __forceinline__ void element_rows_store(const NumArgs &a, const ElemGeo<D> &g, const unsigned (&pos)[4])
 {
     constexpr int VPR = (D + 1) * n_outputs<OPS>() * M * M;
@@ -1222,7 +1170,7 @@ __device__ __forceinline__ void element_rows_store(const NumArgs &a, const ElemG
         general_all_rows<D>(a, g, K);
 #pragma unroll
         for (int al = 0; al <= D; ++al)
-            if (pos[al] != 0xffffffffu) store_row<D + 1, KEEP>(a.kbuf + (int64_t)pos[al] * a.kstride, K[al]);
+            if (pos[al] != 0xffffffffu) store_row<D + 1>(a.kbuf + (int64_t)pos[al] * a.kstride, K[al]);
         return;
     }
     if (pos[A] != 0xffffffffu) {
@@ -1240,7 +1188,7 @@ __device__ __forceinline__ void element_rows_store(const NumArgs &a, const ElemG
             for (int i = 0; i < VPR; ++i) dst[i] = vals[i];
         }
     }
-    if constexpr (A < D) element_rows_store<D, M, OPS, A + 1, KEEP>(a, g, pos);
+    if constexpr (A < D) element_rows_store<D, M, OPS, A + 1>(a, g, pos);
 }
 
 template <int D, int M, int OPS, int CORE, int MINB>
@@ -1308,8 +1256,7 @@ template <int D>
 __global__ void __launch_bounds__(EB_SIZE) k_eb_build(const typename IdxT<D>::type *__restrict__ me, int64_t e_lo,
                                                       int64_t ne, int32_t *__restrict__ verts,
                                                       int32_t *__restrict__ count, uint32_t *__restrict__ loc,
-                                                      unsigned long long *maxn,
-                                                      const int32_t *__restrict__ elist = nullptr)
+                                                      unsigned long long *maxn)
 {
     constexpr int NK = 4 * EB_SIZE;
     __shared__ int keys[NK];
@@ -1318,12 +1265,9 @@ __global__ void __launch_bounds__(EB_SIZE) k_eb_build(const typename IdxT<D>::ty
     const int t = threadIdx.x;
     const int64_t b = blockIdx.x, i = b * EB_SIZE + t;
     int v[D + 1];
-    // (elist: the batches cover a virtual element list; -1 entries are padding)
-    const int64_t e = i < ne ? (elist ? (int64_t)elist[i] : e_lo + i) : -1;
-    const bool have = e >= 0;
-    if (have) load_element<D>(me, e, v);
+    if (i < ne) load_element<D>(me, e_lo + i, v);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) keys[k * EB_SIZE + t] = (have && k <= D) ? v[k < D + 1 ? k : 0] : INT_MAX;
+    for (int k = 0; k < 4; ++k) keys[k * EB_SIZE + t] = (i < ne && k <= D) ? v[k < D + 1 ? k : 0] : INT_MAX;
     __syncthreads();
     // bitonic sort, NK/2 compare pairs per stage
     for (int kk = 2; kk <= NK; kk <<= 1)
@@ -1375,7 +1319,7 @@ __global__ void __launch_bounds__(EB_SIZE) k_eb_build(const typename IdxT<D>::ty
         count[b] = n <= EB_CAP ? n : -1;
         atomicMax(maxn, (unsigned long long)n);   // > EB_CAP: some batch takes the direct path
     }
-    if (have && n <= EB_CAP) {
+    if (i < ne && n <= EB_CAP) {
         unsigned l = 0;
 #pragma unroll
         for (int k = 0; k <= D; ++k) {
@@ -1421,7 +1365,7 @@ __device__ __forceinline__ void element_from_stage(const double *__restrict__ vr
 //   K[a][b] = G_a . Q_b + G_b . R_a + (a == b ? cd : co) ((a0s + a0_a) + a0_b)
 // ~210 fp64 instructions for the 16 entries instead of ~370 in reference
 // order.  Rows go to their incidence slots (pos) as in element_rows_store.
-template <int D, int CORE, bool KEEP = false>
+template <int D, int CORE>
 __device__ __forceinline__ bool stage_general_fast(const NumArgs &a, const double *__restrict__ vrec, unsigned lc,
                                                    double vol, const unsigned (&pos)[4])
 {
@@ -1505,7 +1449,7 @@ __device__ __forceinline__ bool stage_general_fast(const NumArgs &a, const doubl
     }
 #pragma unroll
     for (int al = 0; al <= D; ++al)
-        if (pos[al] != 0xffffffffu) store_row<D + 1, KEEP>(a.kbuf + (int64_t)pos[al] * a.kstride, K[al]);
+        if (pos[al] != 0xffffffffu) store_row<D + 1>(a.kbuf + (int64_t)pos[al] * a.kstride, K[al]);
     return deg;
 }
 
@@ -1523,11 +1467,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// TILED: the batches walk a tile's virtual element list (a.elist: element of
-// each entry, -1 = padding; a.epos: tile-relative slots, ~0u = row outside
-// the tile) and the rows are stored with the default cache policy -- the
-// tile's fold reads them back from L2.
-template <int D, int M, int OPS, int CORE, int MINB, bool FAST = false, bool TILED = false>
+template <int D, int M, int OPS, int CORE, int MINB, bool FAST = false>
 __global__ void __launch_bounds__(EB_SIZE, MINB) k_element_rows_pipe(NumArgs a)
 {
     extern __shared__ double dyn[];
@@ -1574,21 +1514,11 @@ __global__ void __launch_bounds__(EB_SIZE, MINB) k_element_rows_pipe(NumArgs a)
         lc = 0;
         vol = 0.0;
         if (bb < nb && i < a.ne) {
-            if constexpr (TILED) {
-                const int e = __ldcs(a.elist + i);
-                if (e >= 0) {
-                    p = __ldcs(a.epos + i);
-                    lc = __ldcs(a.eb_loc + i);
-                    vol = __ldg(a.vols + e);
-                }
-            } else {
-                p = __ldcs(a.epos + i);
-                lc = __ldcs(a.eb_loc + i);
-                vol = __ldcs(a.vols + a.e_lo + i);
-            }
+            p = __ldcs(a.epos + i);
+            lc = __ldcs(a.eb_loc + i);
+            vol = __ldcs(a.vols + a.e_lo + i);
         }
     };
-    auto elem_of = [&](int64_t i) -> int64_t { return TILED ? (int64_t)a.elist[i] : a.e_lo + i; };
     uint4 p;
     unsigned lc;
     double vol;
@@ -1613,16 +1543,16 @@ __global__ void __launch_bounds__(EB_SIZE, MINB) k_element_rows_pipe(NumArgs a)
         for (int kk = 0; kk <= D; ++kk) any |= pos[kk] != 0xffffffffu;
         if (i < a.ne && any) {
             if constexpr (FAST && OPS == OP_GENERAL) {
-                if (stage_general_fast<D, CORE, TILED>(a, recs + (size_t)(k & 1) * RS, lc, vol, pos))
-                    atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)elem_of(i));
+                if (stage_general_fast<D, CORE>(a, recs + (size_t)(k & 1) * RS, lc, vol, pos))
+                    atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)(a.e_lo + i));
             } else {
                 ElemRaw<D> x;
                 x.vol = vol;
                 element_from_stage<D, OPS>(recs + (size_t)(k & 1) * RS, lc, x);
                 ElemGeo<D> g;
                 if (element_compute<D, OPS, CORE>(x, g))
-                    atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)elem_of(i));
-                element_rows_store<D, M, OPS, 0, TILED>(a, g, pos);
+                    atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)(a.e_lo + i));
+                element_rows_store<D, M, OPS>(a, g, pos);
             }
         }
         p = pn;
@@ -1631,265 +1561,6 @@ __global__ void __launch_bounds__(EB_SIZE, MINB) k_element_rows_pipe(NumArgs a)
         __syncthreads();   // stage k & 1 is rewritten by the records of batch k+2
     }
     cp_async_wait<0>();
-}
-
-// ---------------------------------------------------------------------------
-// Fused tiled two-pass (3D general operator): ONE persistent kernel runs the
-// element pass and the fold of every tile.  Batch g of the global batch list
-// (tiles in order) belongs to CTA g mod G, so the three-stage cp.async
-// pipeline of k_element_rows_pipe runs across tile boundaries without
-// draining; when a CTA's next batch belongs to tile p it first folds its share
-// (chunks of 8 sorted warps, chunk h of the global chunk list to CTA h mod G)
-// of the tiles up to p - 2, whose local rows sit in a ring of TILE_RING tile
-// buffers that stays in L2.  Tiles hand over through two counters per tile
-// (element batches done, fold chunks done): release = __threadfence + atomic
-// after a CTA barrier, acquire = ld.acquire.gpu spin by one thread + barrier;
-// the ring is read with ld.global.cg (L2: its addresses are rewritten every
-// TILE_RING tiles, an L1 line could be stale).  Every wait refers to work of
-// earlier tiles that its owner reaches earlier in its own program order, and
-// all CTAs are resident (grid = occupancy x SMs), so the waits cannot cycle;
-// they are bounded anyway (counters[7] = timeout -> SA_ERR_CUDA).  Same
-// element values and fold order as the two-kernel path: bitwise identical.
-constexpr int TILE_RING = 3;
-constexpr int TILE_FCH = EB_SIZE / 32;   // sorted warps per fold chunk
-
-__device__ __forceinline__ void ld256_cg(const double *p, double &a, double &b, double &c, double &d)
-{
-    asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p) : "memory");
-}
-
-template <int CORE, bool FAST>
-__global__ void __launch_bounds__(EB_SIZE, 2) k_tiled_fused(NumArgs a)
-{
-    constexpr int D = 3;
-    constexpr int OPS = OP_GENERAL;
-    extern __shared__ double dyn[];
-    double *recs = dyn;                                                 // [2][maxn][EB_REC]
-    int *svs = (int *)(dyn + 2 * (size_t)a.eb_maxn * EB_REC);           // [3][EB_CAP + 1] (+ count)
-    double *facc = (double *)(svs + 3 * (EB_CAP + 1));                  // fold accumulators [8 warps][32][acc_stride | 1]
-    const int t = threadIdx.x, lane = t & 31, wp = t >> 5;
-    const int64_t nb = a.eb_b1;   // all batches of all tiles
-    const int64_t G = gridDim.x;
-    const int RS = a.eb_maxn * EB_REC;
-    unsigned long long *abort_flag = (unsigned long long *)(a.counters + 7);
-
-    auto wait_count = [&](const unsigned *ctr, unsigned target) {
-        if (t == 0) {
-            unsigned v;
-            for (int spins = 0;; ++spins) {
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-                if (v >= target) break;
-                if (*(volatile unsigned long long *)abort_flag) break;
-                if (spins > (1 << 21)) { atomicExch(abort_flag, 1ull); break; }
-                __nanosleep(64);
-            }
-        }
-        __syncthreads();
-    };
-    auto signal = [&](unsigned *ctr) {
-        __threadfence();
-        __syncthreads();
-        if (t == 0) atomicAdd(ctr, 1u);
-    };
-
-    // ---- fold of chunk j of tile q (the PRE/TILED path of k_numeric_rowgather, M = 1)
-    auto fold_chunk = [&](int q, int64_t j) {
-        const unsigned full = 0xffffffffu;
-        const int64_t p0 = a.tile_p[q], p1 = a.tile_p[q + 1];
-        const int64_t tpos = p0 + TILE_FCH * j + wp;
-        const int64_t nl = tpos < p1 ? (int64_t)a.tw_order[tpos] * 32 + lane : a.nnodes;
-        const bool in_range = nl < a.nnodes;
-        const int64_t c0 = in_range ? a.colptr[nl] : 0;
-        const int deg_row = in_range ? (int)(a.colptr[nl + 1] - c0) : -1;
-        const bool active = in_range && deg_row <= a.light_deg;
-        const int deg = active ? deg_row : -1;
-        const int64_t row_base = active ? a.indptr[nl] : 0;
-        const int n_inc = active ? (int)(a.inc_ptr[nl + 1] - a.inc_ptr[nl]) : 0;
-        const int d0 = __shfl_sync(full, deg, 0);
-        const bool uniform = __all_sync(full, deg == d0) && d0 > 0;
-        int dmax = deg;
-#pragma unroll
-        for (int sh = 16; sh > 0; sh >>= 1) dmax = max(dmax, __shfl_xor_sync(full, dmax, sh));
-        const int S = uniform ? d0 : (max(dmax, 0) | 1);
-        double *wacc = facc + (size_t)wp * 32 * (a.acc_stride | 1) + lane * S;
-        double rbound = 0.0;
-        int nz = 0;
-        if (active) {
-            for (int k = 0; k < deg; ++k) wacc[k] = 0.0;
-            const int64_t vs = a.tw_vseg[tpos];
-            const unsigned *rk = a.tp_rank + vs + lane;
-            const double *kb = a.kbuf + ((int64_t)(q % TILE_RING) * a.ring_slots + (vs - a.tw_vseg[p0]) + lane) * 4;
-            auto accum = [&](const double(&v)[4], unsigned ranks) {
-                if constexpr (FAST) rbound += fabs(v[0]) + fabs(v[1]) + fabs(v[2]) + fabs(v[3]);
-#pragma unroll
-                for (int b = 0; b < 4; ++b) wacc[(ranks >> (8 * b)) & 0xff] += v[b];
-            };
-            constexpr int U = 4;
-            int k = 0;
-            for (; k + U <= n_inc; k += U) {
-                unsigned r[U];
-                double v[U][4];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    r[u] = __ldcs(rk + 32 * (k + u));
-                    ld256_cg(kb + 128 * (int64_t)(k + u), v[u][0], v[u][1], v[u][2], v[u][3]);
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) accum(v[u], r[u]);
-            }
-            for (; k < n_inc; ++k) {
-                double v[4];
-                const unsigned r = __ldcs(rk + 32 * k);
-                ld256_cg(kb + 128 * (int64_t)k, v[0], v[1], v[2], v[3]);
-                accum(v, r);
-            }
-        }
-        __syncwarp();
-        if constexpr (FAST) {
-            if (active) {
-                bool flag = false;
-                const double thr = SA_GUARD_TAU * rbound;
-                for (int k = 0; k < deg; ++k) flag |= fabs(wacc[k]) <= thr;
-                if (flag) a.flag_rows[atomicAdd(a.nflag, 1)] = (uint32_t)nl;
-            }
-        }
-        if (uniform) {
-            const int64_t base = __shfl_sync(full, row_base, 0);
-            const double *plane = wacc - lane * S;
-            for (int i = lane; i < 32 * S; i += 32) {
-                const double val = plane[i];
-                __stcs(a.vals[0] + base + i, val);
-                if constexpr (!FAST) nz += (val == 0.0);
-            }
-        } else if (active) {
-            for (int k = 0; k < deg; ++k) {
-                const double val = wacc[k];
-                __stcs(a.vals[0] + row_base + k, val);
-                if constexpr (!FAST) nz += (val == 0.0);
-            }
-        }
-        if constexpr (!FAST) {
-#pragma unroll
-            for (int sh = 16; sh > 0; sh >>= 1) nz += __shfl_xor_sync(full, nz, sh);
-            if (lane == 0 && nz) atomicAdd((unsigned long long *)a.counters, (unsigned long long)nz);
-        }
-    };
-    int fnext = 0;   // first tile whose fold chunks this CTA has not done yet
-    auto do_folds = [&](int upto) {
-        if (a.dbg == 1) return;
-        for (; fnext < upto; ++fnext) {
-            const int64_t c0 = a.tile_fc[fnext], c1 = a.tile_fc[fnext + 1];
-            int64_t h = c0 + (((int64_t)blockIdx.x - c0 % G) + G) % G;
-            if (h >= c1) continue;
-            if (a.dbg != 2) wait_count(a.tile_sync + fnext, (unsigned)(a.tile_b[fnext + 1] - a.tile_b[fnext]));
-            for (; h < c1; h += G) {
-                fold_chunk(fnext, h - c0);
-                signal(a.tile_sync + a.nt + fnext);
-            }
-        }
-    };
-
-    // ---- element pass (k_element_rows_pipe over the global batch list)
-    auto issue_list = [&](int64_t bb, int stage) {
-        if (bb >= nb) return;
-        int *sv = svs + stage * (EB_CAP + 1);
-        const int32_t *vl = a.eb_verts + bb * EB_CAP;
-        for (int s = t; s < EB_CAP; s += EB_SIZE) cp_async4(sv + s, vl + s);
-        if (t == 0) cp_async4(sv + EB_CAP, a.eb_count + bb);
-    };
-    auto issue_recs = [&](int64_t bb, int lstage, int rstage) {
-        if (bb >= nb) return;
-        const int *sv = svs + lstage * (EB_CAP + 1);
-        double *rec = recs + (size_t)rstage * RS;
-        const int n = sv[EB_CAP];
-        for (int c = t; c < n * 10; c += EB_SIZE) {
-            const int s = c / 10, h = c - 10 * s;
-            const int64_t vv = sv[s];
-            const double *src = h < 2 ? (const double *)a.qv + vv * 4 + 2 * h : a.gen_packed + vv * 16 + 2 * (h - 2);
-            cp_async16(rec + s * EB_REC + 2 * h, src);
-        }
-    };
-    auto own = [&](int64_t bb, uint4 &p, unsigned &lc, double &vol) {
-        const int64_t i = bb * EB_SIZE + t;
-        p = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
-        lc = 0;
-        vol = 0.0;
-        if (bb < nb) {
-            const int e = __ldcs(a.elist + i);
-            if (e >= 0) {
-                p = __ldcs(a.epos + i);
-                lc = __ldcs(a.eb_loc + i);
-                vol = __ldg(a.vols + e);
-            }
-        }
-    };
-    const int64_t b0 = blockIdx.x;
-    if (b0 < nb && a.dbg != 2) {
-        issue_list(b0, 0);
-        cp_async_commit();
-        issue_list(b0 + G, 1);
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncthreads();
-        issue_recs(b0, 0, 0);
-        cp_async_commit();
-        uint4 p;
-        unsigned lc;
-        double vol;
-        own(b0, p, lc, vol);
-        int tile = -1;
-        unsigned roff = 0;
-        for (int64_t k = 0;; ++k) {
-            const int64_t b = b0 + k * G;
-            if (b >= nb) break;
-            issue_list(b + 2 * G, (int)((k + 2) % 3));
-            cp_async_commit();
-            cp_async_wait<1>();   // records of batch k and the list of batch k+1 have landed
-            __syncthreads();
-            issue_recs(b + G, (int)((k + 1) % 3), (int)((k + 1) & 1));
-            cp_async_commit();
-            uint4 pn;
-            unsigned lcn;
-            double voln;
-            own(b + G, pn, lcn, voln);
-            if (tile < 0 || b >= a.tile_b[tile + 1]) {   // first batch of a new tile (uniform over the CTA)
-                do ++tile; while (b >= a.tile_b[tile + 1]);
-                do_folds(tile - 1);
-                if (tile >= TILE_RING && a.dbg != 1)   // the ring buffer of this tile was read by the folds of tile - TILE_RING
-                    wait_count(a.tile_sync + a.nt + tile - TILE_RING,
-                               (unsigned)(a.tile_fc[tile - TILE_RING + 1] - a.tile_fc[tile - TILE_RING]));
-                roff = (unsigned)((tile % TILE_RING) * a.ring_slots);
-            }
-            const int64_t i = b * EB_SIZE + t;
-            unsigned pos[4] = {p.x, p.y, p.z, p.w};
-            bool any = false;
-#pragma unroll
-            for (int kk = 0; kk <= D; ++kk) {
-                any |= pos[kk] != 0xffffffffu;
-                if (pos[kk] != 0xffffffffu) pos[kk] += roff;
-            }
-            if (any) {
-                if constexpr (FAST) {
-                    if (stage_general_fast<D, CORE, true>(a, recs + (size_t)(k & 1) * RS, lc, vol, pos))
-                        atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)a.elist[i]);
-                } else {
-                    ElemRaw<D> x;
-                    x.vol = vol;
-                    element_from_stage<D, OPS>(recs + (size_t)(k & 1) * RS, lc, x);
-                    ElemGeo<D> g;
-                    if (element_compute<D, OPS, CORE>(x, g))
-                        atomicMin((unsigned long long *)(a.counters + 4), (unsigned long long)a.elist[i]);
-                    element_rows_store<D, 1, OPS, 0, true>(a, g, pos);
-                }
-            }
-            p = pn;
-            lc = lcn;
-            vol = voln;
-            signal(a.tile_sync + tile);   // (its barrier also frees stage k & 1 for the records of batch k+2)
-        }
-        cp_async_wait<0>();
-    }
-    do_folds(a.nt);
 }
 
 // element range of the block's incidences: out[0] = min e, out[1] = max e
@@ -2280,78 +1951,6 @@ int launch_twopass(const sa_plan *P, const NumArgs &a, int64_t nnodes, cudaStrea
     const bool pipe = GEN3 && a.eb_loc && a.gen_packed && a.eb_allfit;
     const bool fast = pipe && !a.exact;
     if constexpr (GEN3) {
-        if (pipe && P->tiled) {
-            // Tiled: per tile, the element pass over the tile's virtual
-            // elements, then the fold of its rows -- the tile's local rows
-            // (a reused ring buffer of at most tile_max_slots rows) never
-            // leave the L2.  Same per-element values, same fold order.
-            auto pk = fast ? k_element_rows_pipe<D, M, OPS, CORE, 2, true, true>
-                           : k_element_rows_pipe<D, M, OPS, CORE, 2, false, true>;
-            void (*fk)(NumArgs) = fast ? k_numeric_rowgather<D, M, OPS, CORE, 2, 1, true, false, true, true>
-                                       : k_numeric_rowgather<D, M, OPS, CORE, 2, 1, true, false, false, true>;
-            const size_t psm = 2 * (size_t)std::max(a.eb_maxn, 1) * EB_REC * sizeof(double) +
-                               3 * (EB_CAP + 1) * sizeof(int);
-            SA_CUDA_TRY(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
-            int dev = 0, nsm = 148, occ = 0;
-            SA_CUDA_TRY(cudaGetDevice(&dev));
-            SA_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-            SA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pk, EB_SIZE, psm));
-            const size_t per_thread = (size_t)NOUT * (a.acc_stride | 1) * sizeof(double);
-            int block = 128;
-            while (per_thread * block > 100 * 1024 && block > 32) block /= 2;
-            const size_t smem = per_thread * block;
-            if (smem > 200 * 1024)
-                return set_error(SA_ERR_CAPACITY, "row accumulators need %zu B of shared memory per %d threads", smem,
-                                 block);
-            SA_CUDA_TRY(cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            if (fast) SA_CUDA_TRY(cudaMemsetAsync(a.nflag, 0, sizeof(int), st));
-            NumArgs b = a;
-            if (tune_int("tile_fused", 1) != 0 && block == 128) {
-                // one persistent kernel for every tile (k_tiled_fused)
-                auto uk = fast ? k_tiled_fused<CORE, true> : k_tiled_fused<CORE, false>;
-                const size_t usm = psm + (size_t)TILE_FCH * 32 * (a.acc_stride | 1) * sizeof(double);
-                SA_CUDA_TRY(cudaFuncSetAttribute(uk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm));
-                int uocc = 0;
-                SA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&uocc, uk, EB_SIZE, usm));
-                if (uocc >= 1) {
-                    SA_CUDA_TRY(cudaMemsetAsync(P->tile_sync, 0, 2 * P->nt * sizeof(unsigned), st));
-                    b.eb_b0 = 0;
-                    b.eb_b1 = P->nv / EB_SIZE;
-                    b.tile_b = P->tile_dev;
-                    b.tile_p = P->tile_dev + (P->nt + 1);
-                    b.tile_fc = P->tile_dev + 2 * (P->nt + 1);
-                    b.tile_sync = P->tile_sync;
-                    b.nt = (int)P->nt;
-                    b.ring_slots = P->tile_max_slots;
-                    b.dbg = tune_int("tile_dbg", 0);
-                    SA_LAUNCH(uk, (unsigned)(nsm * uocc), EB_SIZE, usm, st, b);
-                    if (fast && nnodes) SA_LAUNCH((k_guard_fixup<D, OPS, CORE>), 148, 128, 0, st, a);
-                    return SA_OK;
-                }
-            }
-            const int ns = P->tile_ns;
-            SA_CUDA_TRY(cudaEventRecord(P->tile_ev[ns], st));
-            for (int s = 0; s < ns; ++s) SA_CUDA_TRY(cudaStreamWaitEvent(P->tile_st[s], P->tile_ev[ns], 0));
-            for (int64_t t = 0; t < P->nt; ++t) {
-                cudaStream_t ts = P->tile_st[t % ns];
-                b.kbuf = a.kbuf + (t % ns) * P->tile_max_slots * a.kstride;
-                b.eb_b0 = P->tile_v0[t] / EB_SIZE;
-                b.eb_b1 = P->tile_v0[t + 1] / EB_SIZE;
-                b.tw_p0 = P->tile_w0[t];
-                b.tw_p1 = P->tile_w0[t + 1];
-                const int64_t nb = b.eb_b1 - b.eb_b0;
-                if (nb)
-                    SA_LAUNCH(pk, (unsigned)std::min<int64_t>(nb, (int64_t)nsm * std::max(occ, 1)), EB_SIZE, psm, ts, b);
-                const int64_t nr = 32 * (b.tw_p1 - b.tw_p0);
-                if (nr) SA_LAUNCH(fk, grid_for(nr, block), block, smem, ts, b);
-            }
-            for (int s = 0; s < ns; ++s) {
-                SA_CUDA_TRY(cudaEventRecord(P->tile_ev[s], P->tile_st[s]));
-                SA_CUDA_TRY(cudaStreamWaitEvent(st, P->tile_ev[s], 0));
-            }
-            if (fast && nnodes) SA_LAUNCH((k_guard_fixup<D, OPS, CORE>), 148, 128, 0, st, a);
-            return SA_OK;
-        }
         if (pipe) {
             // (fast: 126 registers, 2 blocks of 256 per SM; batches of 256
             // elements read 7.7 instead of 9.5 GB -- C5 7.77 vs 7.90 ms)
@@ -2540,8 +2139,6 @@ static void free_all(std::initializer_list<void *> ps)
         if (p) cudaFreeAsync(p, 0);
 }
 
-#include "sa_tiles.cuh"
-
 // ===========================================================================
 // C ABI
 
@@ -2620,15 +2217,9 @@ int sa_mesh_destroy(sa_mesh *M)
 int sa_plan_destroy(sa_plan *P)
 {
     if (!P) return SA_OK;
-    for (int s = 0; s < P->tile_ns; ++s) {
-        cudaStreamSynchronize(P->tile_st[s]);
-        cudaStreamDestroy(P->tile_st[s]);
-        cudaEventDestroy(P->tile_ev[s]);
-    }
-    if (P->tile_ns) cudaEventDestroy(P->tile_ev[P->tile_ns]);
     free_all({P->inc_ptr, P->inc, P->winc, P->wseg, P->colptr, P->cols, P->indptr, P->indices, P->counters,
               P->scan_tmp, P->epos, P->kbuf, P->tp_rank, P->eb_verts, P->eb_count, P->eb_loc, P->gd_flag_rows,
-              P->gd_nflag, P->heavy_rows, P->tw_order, P->tw_vseg, P->tv_elem, P->tv_pos, P->tile_dev, P->tile_sync});
+              P->gd_nflag, P->heavy_rows});
     delete P;
     return SA_OK;
 }
@@ -2680,18 +2271,16 @@ int sa_plan_info(const sa_plan *P, int64_t *nrows, int64_t *nnz, int64_t *max_ro
 int sa_plan_stats(const sa_plan *P, int64_t *out, int n)
 {
     if (!P || !out) return set_error(SA_ERR_ARG, "plan/out is NULL");
-    const int64_t nn = P->nnodes, nw = (nn + 31) / 32, ne = P->tiled ? P->nv : P->e_hi - P->e_lo,
-                  nb = (ne + EB_SIZE - 1) / EB_SIZE;
+    const int64_t nn = P->nnodes, nw = (nn + 31) / 32, ne = P->e_hi - P->e_lo, nb = (ne + EB_SIZE - 1) / EB_SIZE;
     // device bytes of the plan's symbolic structures (pattern, incidences,
     // warp records, two-pass slot map / row buffer / element batches)
     const int64_t bytes = 3 * (nn + 1) * 8 + P->n_inc * 8 + P->n_colnodes * 4 + (P->nrows + 1) * 8 + P->nnz * 4 +
                           P->n_winc * (int64_t)sizeof(IncRec) + (P->wseg ? (nw + 1) * 8 : 0) +
                           (P->epos ? ne * 16 : 0) + P->kbuf_elems * 8 + P->tp_nslots * 4 +
-                          (P->eb_loc ? ne * 4 + nb * (EB_CAP + 1) * 4 : 0) +
-                          (P->tiled ? P->nv * 20 + (2 * nw + 1) * 8 : 0);
-    const int64_t v[13] = {P->n_inc, P->max_deg, P->nnodes, P->nnz, P->n_winc, P->tp_nslots, P->eb_allfit ? 1 : 0,
-                           P->eb_maxn, bytes, P->light_deg, P->n_heavy, P->tiled ? P->nt : 0, P->tiled ? P->nv : 0};
-    for (int i = 0; i < n && i < 13; ++i) out[i] = v[i];
+                          (P->eb_loc ? ne * 4 + nb * (EB_CAP + 1) * 4 : 0);
+    const int64_t v[11] = {P->n_inc, P->max_deg, P->nnodes, P->nnz, P->n_winc, P->tp_nslots, P->eb_allfit ? 1 : 0,
+                           P->eb_maxn, bytes, P->light_deg, P->n_heavy};
+    for (int i = 0; i < n && i < 11; ++i) out[i] = v[i];
     return SA_OK;
 }
 
@@ -2722,7 +2311,7 @@ static bool want_twopass(int ops, int d, int m)
 // (built on first use, kept with the plan)
 static int ensure_twopass(sa_plan *P, int kstride, bool batches, cudaStream_t st)
 {
-    if (!P->epos && !P->tiled) {
+    if (!P->epos) {
         unsigned long long h[2] = {0xffffffffull, 0};
         unsigned long long *dr = nullptr;
         SA_CUDA_TRY(cudaMallocAsync((void **)&dr, 2 * sizeof(unsigned long long), st));
@@ -2737,35 +2326,25 @@ static int ensure_twopass(sa_plan *P, int kstride, bool batches, cudaStream_t st
         P->e_hi = P->n_inc ? (int64_t)h[1] + 1 : 0;
         const int64_t ne = P->e_hi - P->e_lo;
         const int64_t nn = P->nnodes, nw = (nn + 31) / 32;
-        int64_t *span = nullptr;
-        SA_CUDA_TRY(cudaMallocAsync((void **)&span, (nw + 1) * sizeof(int64_t), st));
-        if (nw) SA_LAUNCH(k_warp_span, grid_for(nw, 128), 128, 0, st, P->inc_ptr, nn, span);
-        // tiled schedule (3D general operator, coordinates known): the local
-        // rows of a tile stay in L2 (sa_tiles.cuh); SA_TUNE tile_kb = ring
-        // buffer budget, 0 = untiled
-        const int tile_kb = tune_int("tile_kb", 32 * 1024);
-        if (batches && P->mesh->d == 3 && !P->tile_tried && tile_kb > 0) {
-            const int rc = build_tiles(P, span, std::max<int64_t>((int64_t)tile_kb * 1024 / (kstride * 8), 32), st);
-            if (rc != SA_OK) { cudaFreeAsync(span, st); return rc; }
+        if (!P->wseg) {   // warp-interleaved slot offsets (built with winc in 3D)
+            int64_t *span = nullptr;
+            SA_CUDA_TRY(cudaMallocAsync((void **)&span, (nw + 1) * sizeof(int64_t), st));
+            SA_CUDA_TRY(cudaMallocAsync((void **)&P->wseg, (nw + 1) * sizeof(int64_t), st));
+            if (nw) SA_LAUNCH(k_warp_span, grid_for(nw, 128), 128, 0, st, P->inc_ptr, nn, span);
+            SA_TRY(exclusive_scan_i64(span, P->wseg, nw, P->scan_tmp, st));
+            SA_CUDA_TRY(cudaFreeAsync(span, st));
         }
-        if (!P->tiled) {
-            if (!P->wseg) {   // warp-interleaved slot offsets (built with winc in 3D)
-                SA_CUDA_TRY(cudaMallocAsync((void **)&P->wseg, (nw + 1) * sizeof(int64_t), st));
-                SA_TRY(exclusive_scan_i64(span, P->wseg, nw, P->scan_tmp, st));
-            }
-            SA_CUDA_TRY(cudaMemcpyAsync(&P->tp_nslots, P->wseg + nw, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-            SA_CUDA_TRY(cudaStreamSynchronize(st));
-            if (P->tp_nslots >= 0xffffffffLL)
-                return set_error(SA_ERR_CAPACITY, "two-pass numeric: %lld slots overflow 32-bit slot indices",
-                                 (long long)P->tp_nslots);
-            SA_CUDA_TRY(cudaMallocAsync((void **)&P->epos, std::max<int64_t>(ne, 1) * sizeof(uint4), st));
-            SA_CUDA_TRY(cudaMemsetAsync(P->epos, 0xff, std::max<int64_t>(ne, 1) * sizeof(uint4), st));
-            SA_CUDA_TRY(cudaMallocAsync((void **)&P->tp_rank, std::max<int64_t>(P->tp_nslots, 1) * sizeof(unsigned), st));
-            if (nn)
-                SA_LAUNCH(k_tp_slots, grid_for(nn, 128), 128, 0, st, P->inc_ptr, P->inc, nn, P->wseg, (unsigned)P->e_lo,
-                          (unsigned *)P->epos, P->tp_rank);
-        }
-        SA_CUDA_TRY(cudaFreeAsync(span, st));
+        SA_CUDA_TRY(cudaMemcpyAsync(&P->tp_nslots, P->wseg + nw, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        if (P->tp_nslots >= 0xffffffffLL)
+            return set_error(SA_ERR_CAPACITY, "two-pass numeric: %lld slots overflow 32-bit slot indices",
+                             (long long)P->tp_nslots);
+        SA_CUDA_TRY(cudaMallocAsync((void **)&P->epos, std::max<int64_t>(ne, 1) * sizeof(uint4), st));
+        SA_CUDA_TRY(cudaMemsetAsync(P->epos, 0xff, std::max<int64_t>(ne, 1) * sizeof(uint4), st));
+        SA_CUDA_TRY(cudaMallocAsync((void **)&P->tp_rank, std::max<int64_t>(P->tp_nslots, 1) * sizeof(unsigned), st));
+        if (nn)
+            SA_LAUNCH(k_tp_slots, grid_for(nn, 128), 128, 0, st, P->inc_ptr, P->inc, nn, P->wseg, (unsigned)P->e_lo,
+                      (unsigned *)P->epos, P->tp_rank);
     }
     if (batches && !P->eb_loc && P->mesh->d == 3) {
         const int64_t ne = P->e_hi - P->e_lo, nb = (ne + EB_SIZE - 1) / EB_SIZE;
@@ -2789,16 +2368,7 @@ static int ensure_twopass(sa_plan *P, int kstride, bool batches, cudaStream_t st
         SA_CUDA_TRY(cudaMallocAsync((void **)&P->gd_flag_rows, std::max<int64_t>(P->nnodes, 1) * sizeof(uint32_t), st));
         SA_CUDA_TRY(cudaMallocAsync((void **)&P->gd_nflag, sizeof(int), st));
     }
-    if (P->tiled && !P->tile_ns) {
-        const int ns = std::min(8, std::max(1, tune_int("tile_streams", 3)));
-        for (int s = 0; s < ns; ++s) {
-            SA_CUDA_TRY(cudaStreamCreateWithFlags(&P->tile_st[s], cudaStreamNonBlocking));
-            SA_CUDA_TRY(cudaEventCreateWithFlags(&P->tile_ev[s], cudaEventDisableTiming));
-        }
-        SA_CUDA_TRY(cudaEventCreateWithFlags(&P->tile_ev[ns], cudaEventDisableTiming));
-        P->tile_ns = ns;
-    }
-    const int64_t kelems = (int64_t)kstride * (P->tiled ? std::max(P->tile_ns, TILE_RING) * P->tile_max_slots : P->tp_nslots);
+    const int64_t kelems = (int64_t)kstride * P->tp_nslots;
     if (P->kbuf_elems < kelems) {
         if (P->kbuf) SA_CUDA_TRY(cudaFreeAsync(P->kbuf, st));
         P->kbuf = nullptr;
@@ -2901,14 +2471,6 @@ int sa_numeric(sa_plan *P, int ops, const sa_coeffs *cf, double *const *vals_dev
         a.epos = P->epos;
         a.e_lo = P->e_lo;
         a.ne = P->e_hi - P->e_lo;
-        if (P->tiled) {   // virtual element lists and tile-relative slots (sa_tiles.cuh)
-            a.epos = P->tv_pos;
-            a.elist = P->tv_elem;
-            a.e_lo = 0;
-            a.ne = P->nv;
-            a.tw_order = P->tw_order;
-            a.tw_vseg = P->tw_vseg;
-        }
         a.tp_rank = P->tp_rank;
         a.wseg = P->wseg;
         a.nflag = P->gd_nflag;

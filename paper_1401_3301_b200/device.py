@@ -157,11 +157,10 @@ class Plan:
         return self._h
 
     def stats(self) -> dict:
-        out = (ctypes.c_int64 * 13)()
-        _lib.check(_lib.load().sa_plan_stats(self._h, out, 13))
+        out = (ctypes.c_int64 * 11)()
+        _lib.check(_lib.load().sa_plan_stats(self._h, out, 11))
         keys = ("incidences", "max_row_nodes", "nodes", "nnz", "warp_records", "twopass_slots",
-                "element_batches_staged", "max_batch_vertices", "device_bytes", "light_row_nodes", "heavy_rows",
-                "tiles", "tile_elements")
+                "element_batches_staged", "max_batch_vertices", "device_bytes", "light_row_nodes", "heavy_rows")
         return dict(zip(keys, [int(x) for x in out]))
 
     def pattern(self, stream=None):

@@ -714,96 +714,3 @@ def test_general_fast_row_blocks_stitch(cuda_ok):
         blocks.append((rb, re_, b.row_ptr, b.col_idx, b.vals))
     rp, ci, va = parallel.stitch(blocks, nq, nq)
     assert_csr_equal(P.SparseMatrix(nq, nq, rp, ci, va), *_oracle(mesh, "general", **f), bitwise=False)
-
-
-def _plan_general(mesh, k):
-    """(stats, indptr, indices, vals, zero count) of one general-operator
-    assembly through a fresh device mesh and plan (no plan cache)."""
-    from paper_1401_3301_b200.device import DeviceMesh
-
-    dm = DeviceMesh(mesh.q, mesh.me, mesh.vols)
-    try:
-        plan = dm.plan(1)
-        plan.prepare([k])
-        st = plan.stats()
-        vals, zeros = plan.numeric([k])
-        ip, ix = plan.pattern()
-        return st, ip.cpu().numpy(), ix.cpu().numpy(), vals[0].cpu().numpy().copy(), zeros[0]
-    finally:
-        dm.close()
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("fused", [1, 0])
-@pytest.mark.parametrize("exact", [True, False])
-@pytest.mark.parametrize("tile_kb", [8, 64, 1024])
-def test_general_tiled_bitwise_untiled(cuda_ok, tile_kb, exact, fused, monkeypatch):
-    # tiled two-pass (sa_tiles.cuh): rows grouped into L2-sized spatial tiles,
-    # each tile's elements (halo included) computed into a reused ring
-    # buffer and folded at once.  Same element values, same fold order:
-    # bitwise the untiled two-pass, whatever the tile size (8 KB: every warp
-    # of 32 rows is its own oversized tile)
-    mesh = _jittered(3, 20, 14013305)
-    f = _c5_fields(mesh.q.shape[1], 14013305)
-    k = P.GeneralKernel(mesh, exact=exact, **f)
-    tune(monkeypatch, tile_kb=0)
-    st0, ip0, ix0, v0, z0 = _plan_general(mesh, k)
-    assert st0["tiles"] == 0
-    # fused: one persistent kernel for all tiles (default); 0: one element-pass
-    # and one fold launch per tile, round-robin on internal streams
-    tune(monkeypatch, tile_kb=tile_kb, tile_maxf=1000, tile_fused=fused)
-    st, ip, ix, v, z = _plan_general(mesh, k)
-    assert st["tiles"] >= 2 and st["tile_elements"] >= mesh.me.shape[1]
-    assert np.array_equal(ip, ip0) and np.array_equal(ix, ix0) and z == z0
-    assert np.array_equal(v.view(np.int64), v0.view(np.int64))
-    got = P.assemble_b200(P.Mesh(mesh.q, mesh.me, mesh.vols), k)
-    assert_csr_equal(got, *_oracle(mesh, "general", **f), bitwise=exact)
-
-
-@pytest.mark.gpu
-def test_general_tiled_guard_hub_and_blocks(cuda_ok, monkeypatch):
-    # tiles with the zero guard (unjittered A = I: thousands of exact
-    # cancellations), on a row block (elements outside the block, rows of
-    # other blocks), and a mesh without numbering locality (halos too large:
-    # the plan keeps the untiled path)
-    from oracle import oracle as O
-
-    tune(monkeypatch, tile_kb=64, tile_maxf=300)
-    q, me = P.hypercube_arrays(3, 12)
-    mesh = P.Mesh(q, me, O.volumes(q, me))
-    nq = q.shape[1]
-    k = P.GeneralKernel(mesh, A=np.eye(3))
-    z = dict(A=np.broadcast_to(np.eye(3), (nq, 3, 3)), b=np.zeros((nq, 3)), c=np.zeros((nq, 3)), a0=np.zeros(nq))
-    rp, ci, va = _oracle(mesh, "general", **z)
-    st, ip, ix, v, nz = _plan_general(mesh, k)
-    assert st["tiles"] >= 2 and nz == len(v) - len(va) > 0
-    assert_csr_equal(P.assemble_b200(mesh, k), rp, ci, va, bitwise=False)
-    # row blocks stitched
-    mesh = _jittered(3, 14, 5)
-    f = _c5_fields(mesh.q.shape[1], 5)
-    k = P.GeneralKernel(mesh, exact=True, **f)
-    rp, ci, va = _oracle(mesh, "general", **f)
-    nq = mesh.q.shape[1]
-    cuts = [0, nq // 3 + 5, 2 * nq // 3 - 7, nq]
-    from paper_1401_3301_b200 import parallel
-    from paper_1401_3301_b200.assembly import assemble_block_b200
-
-    blocks = []
-    for i in range(3):
-        (b,) = assemble_block_b200(mesh, [k], cuts[i], cuts[i + 1])
-        blocks.append((cuts[i], cuts[i + 1], b.row_ptr, b.col_idx, b.vals))
-    srp, sci, sva = parallel.stitch(blocks, nq, nq)
-    assert_csr_equal(P.SparseMatrix(nq, nq, srp, sci, sva), rp, ci, va, bitwise=True)
-    # shuffled numbering: tiles would recompute most elements 4x
-    rng = np.random.default_rng(1)
-    perm = rng.permutation(nq)
-    inv = np.empty_like(perm)
-    inv[perm] = np.arange(nq)
-    m2 = P.Mesh(np.ascontiguousarray(mesh.q[:, perm]), inv[mesh.me], mesh.vols)
-    f2 = {n: np.ascontiguousarray(a[perm]) for n, a in f.items()}
-    k2 = P.GeneralKernel(m2, exact=True, **f2)
-    st2, ip2, ix2, v2, _ = _plan_general(m2, k2)
-    assert st2["tiles"] == 0
-    rp2, ci2, va2 = _oracle(m2, "general", **f2)
-    assert np.array_equal(ip2, rp2) and np.array_equal(ix2, ci2)
-    assert np.array_equal(v2.view(np.int64), va2.view(np.int64))
