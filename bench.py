@@ -587,6 +587,8 @@ def run_e2e(q, me, vols, kernels, rb, re_, col_offset, nme_global, args, world, 
     pv = torch.from_numpy(np.asarray(vols)).pin_memory()
     mesh = P.Mesh(pq.numpy(), pme.numpy(), pv.numpy())
     h2d = pq.numel() * 8 + pme.numel() * 8 + pv.numel() * 8
+    if all(k.op == "general" and not getattr(k, "exact", False) for k in kernels):
+        h2d -= pv.numel() * 8   # fast general operator: volumes recomputed on the device, not uploaded
     # plus the nodal coefficient arrays every assembly uploads (pinned copies
     # cached on the descriptors)
     for k in kernels:

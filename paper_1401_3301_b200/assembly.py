@@ -183,6 +183,12 @@ def assemble_block_b200(mesh, kernels, row_begin: int, row_end: int, core: str =
     main = torch.cuda.current_stream()
     med = torch.as_tensor(np.asarray(mesh.me)).to(main.device, non_blocking=True)
     vols = getattr(mesh, "vols", None)
+    # the fast general operator (values within 1e-12, exact pattern) does not
+    # need the host volumes bit for bit: they are recomputed on the device
+    # from the coordinates (numpy-det factorisation, a few ulp from
+    # mesh.vols) instead of crossing PCIe
+    if all(k.op == "general" and not getattr(k, "exact", False) for k in kernels):
+        vols = None
     vd = torch.as_tensor(np.asarray(vols)).to(main.device, non_blocking=True) if vols is not None else None
     me_done = torch.cuda.Event()
     me_done.record(main)
@@ -197,6 +203,10 @@ def assemble_block_b200(mesh, kernels, row_begin: int, row_end: int, core: str =
     dm = DeviceMesh(None, med, vd, core=core, nq=int(np.asarray(mesh.q).shape[1]))
     t1 = time.perf_counter()
     plan = dm.plan(kernels[0].m, row_begin, row_end)
+    # the kernel-specific plan data (two-pass slot map, element batches) needs
+    # the connectivity only: built while the coefficients still upload
+    if vd is not None or kernels[0].op == "general":
+        plan.prepare(kernels)
     main.wait_stream(side)
     dm.set_coords(qd)
     # the structural pattern downloads while the numeric phase runs
