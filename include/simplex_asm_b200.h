@@ -77,6 +77,14 @@ int sa_mesh_create(int d, int64_t nq, int64_t nme, const double *q_dev, const in
  * vols (as sa_mesh_create would).  sa_numeric fails until they are set. */
 int sa_mesh_set_coords(sa_mesh *mesh, const double *q_dev, const double *vols_dev, void *stream);
 int sa_mesh_vols(const sa_mesh *mesh, double *vols_dev_out, void *stream);
+/* Mesh.validate's volume checks (reference mesh.py:92-101) on the device:
+ * volumes are recomputed from the coordinates (numpy-det factorisation) and
+ * compared with the stored ones (vols_dev, nme).  Outputs the first element
+ * with a non-positive stored volume and the first whose stored volume is off
+ * its recomputed one by more than 1e-12 relative (-1 = none).  The index
+ * range check is sa_mesh_create's (SA_ERR_INDEX_RANGE). */
+int sa_mesh_validate(const sa_mesh *mesh, const double *vols_dev, int64_t *first_nonpositive,
+                     int64_t *first_mismatch, void *stream);
 int sa_mesh_destroy(sa_mesh *mesh);
 
 /* ---- symbolic phase (once per mesh and row block) ---------------------- */

@@ -1694,6 +1694,44 @@ int mesh_coords(sa_mesh *M, const double *q, const double *vols, cudaStream_t st
     return SA_OK;
 }
 
+// volumes recomputed from the coordinates into `out` (Mesh.validate; a
+// degenerate element gives 0.0 there, no error)
+template <int D>
+int mesh_recompute_vols(const sa_mesh *M, double *out, cudaStream_t st)
+{
+    typedef typename VecT<D>::type V;
+    typedef typename IdxT<D>::type I;
+    if (!M->nme) return SA_OK;
+    unsigned long long *bad = (unsigned long long *)M->scratch + 1;
+    const unsigned ge = std::min<int64_t>(grid_for(M->nme, 256), 148 * 32);
+    if (M->core == CORE_SKYLAKEX)
+        SA_LAUNCH((k_volumes<D, CORE_SKYLAKEX>), ge, 256, 0, st, (const V *)M->qv, (const I *)M->me, M->nme, out, bad);
+    else
+        SA_LAUNCH((k_volumes<D, CORE_HASWELL>), ge, 256, 0, st, (const V *)M->qv, (const I *)M->me, M->nme, out, bad);
+    return SA_OK;
+}
+
+// first element with a non-positive stored volume, first element whose stored
+// volume is off its recomputed one by more than 1e-12 relative (mesh.py:92-101)
+__global__ void k_validate_vols(const double *__restrict__ stored, const double *__restrict__ recomputed, int64_t n,
+                                unsigned long long *out)
+{
+    unsigned long long np = ~0ull, mm = ~0ull;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const double v = stored[k], r = recomputed[k];
+        if (v <= 0.0) np = min(np, (unsigned long long)k);
+        if (fabs(v - r) > 1e-12 * r) mm = min(mm, (unsigned long long)k);
+    }
+    for (int sh = 16; sh > 0; sh >>= 1) {
+        np = min(np, __shfl_xor_sync(0xffffffffu, np, sh));
+        mm = min(mm, __shfl_xor_sync(0xffffffffu, mm, sh));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (np != ~0ull) atomicMin(out, np);
+        if (mm != ~0ull) atomicMin(out + 1, mm);
+    }
+}
+
 template <int D>
 int symbolic_kernels(sa_plan *P, cudaStream_t st)
 {
@@ -2097,7 +2135,14 @@ int sa_dispatch_d1(const sa_plan *, const NumArgs &, int, int, cudaStream_t);
 int sa_dispatch_d2(const sa_plan *, const NumArgs &, int, int, cudaStream_t);
 int sa_dispatch_d3(const sa_plan *, const NumArgs &, int, int, cudaStream_t);
 int sa_winc_d3(sa_plan *, cudaStream_t);
+int sa_mesh_revols_d1(const sa_mesh *, double *, cudaStream_t);
+int sa_mesh_revols_d2(const sa_mesh *, double *, cudaStream_t);
+int sa_mesh_revols_d3(const sa_mesh *, double *, cudaStream_t);
 #ifdef SA_D
+int SA_CAT(sa_mesh_revols_d, SA_D)(const sa_mesh *M, double *out, cudaStream_t st)
+{
+    return mesh_recompute_vols<SA_D>(M, out, st);
+}
 #if SA_D == 3
 int sa_winc_d3(sa_plan *P, cudaStream_t st) { return build_winc<3>(P, st); }
 #endif
@@ -2203,6 +2248,36 @@ int sa_mesh_vols(const sa_mesh *M, double *vols_dev_out, void *stream)
     if (!M) return set_error(SA_ERR_ARG, "mesh is NULL");
     SA_CUDA_TRY(cudaMemcpyAsync(vols_dev_out, M->vols, M->nme * sizeof(double), cudaMemcpyDeviceToDevice,
                                 (cudaStream_t)stream));
+    return SA_OK;
+}
+
+int sa_mesh_validate(const sa_mesh *M, const double *vols_dev, int64_t *first_nonpositive, int64_t *first_mismatch,
+                     void *stream)
+{
+    if (!M || !vols_dev || !first_nonpositive || !first_mismatch) return set_error(SA_ERR_ARG, "NULL argument");
+    if (!M->coords) return set_error(SA_ERR_ARG, "mesh coordinates not set (sa_mesh_set_coords)");
+    SA_TRY(set_device(M->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    *first_nonpositive = *first_mismatch = -1;
+    if (!M->nme) return SA_OK;
+    double *re = nullptr;
+    unsigned long long *out = nullptr, h[2] = {~0ull, ~0ull};
+    SA_CUDA_TRY(cudaMallocAsync((void **)&re, M->nme * sizeof(double), st));
+    SA_CUDA_TRY(cudaMallocAsync((void **)&out, sizeof h, st));
+    SA_CUDA_TRY(cudaMemcpyAsync(out, h, sizeof h, cudaMemcpyHostToDevice, st));
+    int rc = M->d == 1 ? sa_mesh_revols_d1(M, re, st) : (M->d == 2 ? sa_mesh_revols_d2(M, re, st) : sa_mesh_revols_d3(M, re, st));
+    if (rc == SA_OK) {
+        k_validate_vols<<<std::min<int64_t>(grid_for(M->nme, 256), 148 * 16), 256, 0, st>>>(vols_dev, re, M->nme, out);
+        err_state().launches++;
+        if (cudaMemcpyAsync(h, out, sizeof h, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            rc = set_error(SA_ERR_CUDA, "volume validation failed: %s", cudaGetErrorString(cudaGetLastError()));
+    }
+    cudaFreeAsync(re, st);
+    cudaFreeAsync(out, st);
+    if (rc != SA_OK) return rc;
+    if (h[0] != ~0ull) *first_nonpositive = (int64_t)h[0];
+    if (h[1] != ~0ull) *first_mismatch = (int64_t)h[1];
     return SA_OK;
 }
 

@@ -93,6 +93,18 @@ class DeviceMesh:
         _lib.check(_lib.load().sa_mesh_vols(self._h, _ptr(out), _stream_ptr(stream)))
         return out
 
+    def validate_vols(self, vols, stream=None) -> tuple[int, int]:
+        """(first element with a non-positive stored volume, first element
+        whose stored volume disagrees with its coordinates by more than 1e-12
+        relative); -1 = none.  The volumes are recomputed on the device
+        (sa_mesh_validate; reference mesh.py:92-101)."""
+        with torch.cuda.device(self.device):
+            vd = _to_dev(vols, torch.float64, self.device)
+            a, b = ctypes.c_int64(), ctypes.c_int64()
+            _lib.check(_lib.load().sa_mesh_validate(self._h, _ptr(vd), ctypes.byref(a), ctypes.byref(b),
+                                                    _stream_ptr(stream)))
+        return a.value, b.value
+
     def plan(self, m: int = 1, row_begin: int = 0, row_end: int | None = None, stream=None) -> "Plan":
         if row_end is None:
             row_end = m * self.nq

@@ -714,3 +714,36 @@ def test_general_fast_row_blocks_stitch(cuda_ok):
         blocks.append((rb, re_, b.row_ptr, b.col_idx, b.vals))
     rp, ci, va = parallel.stitch(blocks, nq, nq)
     assert_csr_equal(P.SparseMatrix(nq, nq, rp, ci, va), *_oracle(mesh, "general", **f), bitwise=False)
+
+
+def test_mesh_validate_on_device(cuda_ok):
+    # Mesh.validate (reference mesh.py:72-101): same checks, order and
+    # messages, index range and volume recomputation on the device
+    from paper_1401_3301_b200.errors import IndexRangeError, MeshValidationError
+
+    mesh = _jittered(3, 6, 11)
+    mesh.validate()
+    _jittered(2, 9, 12).validate()
+    P.Mesh(*P.hypercube_arrays(1, 7), np.full(7, 1.0 / 7)).validate()
+    me = mesh.me.copy()
+    me[2, 17] = mesh.q.shape[1]
+    me[3, 5] = -1
+    with pytest.raises(IndexRangeError, match=r"me\[2, 17\] out of range \[0, 343\)"):
+        P.Mesh(mesh.q, me, mesh.vols).validate()
+    with pytest.raises(MeshValidationError, match=r"connectivity shape \(3, 1296\) does not match \(4, nme\)"):
+        P.Mesh(mesh.q, mesh.me[:3], mesh.vols).validate()
+    with pytest.raises(MeshValidationError, match=r"volume array shape \(5,\) does not match \(nme,\)"):
+        P.Mesh(mesh.q, mesh.me, mesh.vols[:5]).validate()
+    v = mesh.vols.copy()
+    v[40] = 0.0
+    v[77] = -v[77]
+    with pytest.raises(MeshValidationError, match="volume of simplex 40 is not positive"):
+        P.Mesh(mesh.q, mesh.me, v).validate()
+    v = mesh.vols.copy()
+    v[123] *= 1.0 + 3e-12
+    v[500] *= 2.0
+    with pytest.raises(MeshValidationError, match="stored volume of simplex 123 disagrees with its coordinates"):
+        P.Mesh(mesh.q, mesh.me, v).validate()
+    v = mesh.vols.copy()
+    v[9] *= 1.0 + 2e-13    # inside the tolerance
+    P.Mesh(mesh.q, mesh.me, v).validate()
