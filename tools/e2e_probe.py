@@ -38,17 +38,17 @@ def main(name="C5"):
         mark("up_me_vols")
         qd = pq.to(dev, non_blocking=True)
         order = sorted(kernels, key=lambda k: D.OP_BITS[k.op])
-        coeffs = D.upload_coeffs(order, dev, 3)
+        coeffs = D.upload_coeffs(order, dev, q.shape[0])
         mark("up_q_coeffs")
         dm = D.DeviceMesh(None, med, vd, nq=q.shape[1])
         mark("mesh_create")
-        plan = dm.plan(1)
+        plan = dm.plan(kernels[0].m)
         mark("symbolic")
         dm.set_coords(qd)
         mark("set_coords")
         plan.prepare(kernels)
         mark("prepare")
-        pat = _PatternDownload(*plan.pattern(), 0, q.shape[1])
+        pat = _PatternDownload(*plan.pattern(), 0, kernels[0].m * q.shape[1])
         mark("pattern_dl")
         vals, zeros = plan.numeric(kernels, coeffs=coeffs)
         mark("numeric")
