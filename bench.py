@@ -629,6 +629,7 @@ def run_e2e(q, me, vols, kernels, rb, re_, col_offset, nme_global, args, world, 
     return {"value": nme_global / float(t.item()), "unit": "elements/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": float(t.item()) * 1e3,
             "stages_ms": {k: v / steps for k, v in stages.items()},
+            "calls_ms": [round(1e3 * x, 2) for x in times],
             "path": "assemble_block_b200(Mesh(pinned q, me, vols)): upload -> symbolic -> numeric (pattern "
                     "download overlapped) -> compact -> pinned host CSR (indices cross PCIe as int32, widened to "
                     "int64 on the host while the values transfer)",

@@ -1601,28 +1601,69 @@ __global__ void k_tp_slots(const int64_t *__restrict__ inc_ptr, const uint2 *__r
     }
 }
 
-// compaction (K5): drop exact-zero entries (sparse.py:108-111)
-__global__ void k_row_nonzeros(const int64_t *__restrict__ indptr, const double *__restrict__ vals, int64_t nrows,
-                               int64_t *__restrict__ cnt)
+// compaction (K5): drop exact-zero entries (sparse.py:108-111).  Exact zeros
+// are rare, so the passes are streaming: every entry is read coalesced once to
+// find the zeros (each one looks its row up by binary search and bumps the
+// row's counter), and once more by a warp-per-32-rows stream compaction whose
+// output offset is the scanned zero count -- no per-row strided walks.
+__global__ void k_zero_rows(const int64_t *__restrict__ indptr, const double *__restrict__ vals, int64_t nnz,
+                            int64_t nrows, unsigned long long *__restrict__ zcnt)
 {
-    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r >= nrows) return;
-    int64_t c = 0;
-    for (int64_t p = indptr[r]; p < indptr[r + 1]; ++p) c += (vals[p] != 0.0);
-    cnt[r] = c;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x) {
+        if (vals[p] != 0.0) continue;
+        int64_t lo = 0, hi = nrows;   // last row r with indptr[r] <= p
+        while (hi - lo > 1) { const int64_t mid = (lo + hi) >> 1; if (indptr[mid] <= p) lo = mid; else hi = mid; }
+        atomicAdd(zcnt + lo, 1ull);
+    }
+}
+
+__global__ void k_new_ptr(const int64_t *__restrict__ indptr, const int64_t *__restrict__ zpre, int64_t nrows,
+                          int64_t *__restrict__ out)
+{
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r <= nrows) out[r] = indptr[r] - zpre[r];
 }
 
 __global__ void k_compact(const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
                           const double *__restrict__ vals, int64_t nrows, const int64_t *__restrict__ new_ptr,
                           int32_t *__restrict__ out_idx, double *__restrict__ out_val)
 {
-    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (r >= nrows) return;
-    int64_t w = new_ptr[r];
-    for (int64_t p = indptr[r]; p < indptr[r + 1]; ++p) {
-        double v = vals[p];
-        if (v != 0.0) { out_idx[w] = indices[p]; out_val[w] = v; ++w; }
+    const int lane = threadIdx.x & 31;
+    const int64_t r0 = 32 * ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    if (r0 >= nrows) return;
+    const int64_t e0 = indptr[r0], e1 = indptr[min(r0 + 32, nrows)];
+    int64_t w = new_ptr[r0];
+    for (int64_t p = e0 + lane; p - lane < e1; p += 32) {
+        const bool in = p < e1;
+        const double v = in ? vals[p] : 0.0;
+        const int32_t c = in ? indices[p] : 0;
+        const bool keep = in && v != 0.0;
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+            const int64_t q = w + __popc(m & ((1u << lane) - 1));
+            out_idx[q] = c;
+            out_val[q] = v;
+        }
+        w += __popc(m);
     }
+}
+
+// canonical CSR from a structural one (shared by sa_compact / sa_pk_compact)
+inline int compact_csr(const int64_t *indptr, const int32_t *indices, const double *vals, int64_t nr, int64_t nnz,
+                       int64_t *scan_tmp, int64_t *indptr_out, int32_t *indices_out, double *vals_out, cudaStream_t st)
+{
+    int64_t *cnt = nullptr;
+    SA_CUDA_TRY(cudaMallocAsync((void **)&cnt, (nr + 1) * sizeof(int64_t), st));
+    SA_CUDA_TRY(cudaMemsetAsync(cnt, 0, (nr + 1) * sizeof(int64_t), st));
+    if (nr && nnz)
+        SA_LAUNCH(k_zero_rows, std::min<int64_t>(grid_for(nnz, 256), 148 * 16), 256, 0, st, indptr, vals, nnz, nr,
+                  (unsigned long long *)cnt);
+    SA_TRY(exclusive_scan_i64(cnt, cnt, nr, scan_tmp, st));
+    SA_LAUNCH(k_new_ptr, grid_for(nr + 1, 256), 256, 0, st, indptr, cnt, nr, indptr_out);
+    if (nr) SA_LAUNCH(k_compact, grid_for(nr, 256), 256, 0, st, indptr, indices, vals, nr, indptr_out, indices_out,
+                      vals_out);
+    SA_CUDA_TRY(cudaFreeAsync(cnt, st));
+    return SA_OK;
 }
 
 // ---------------------------------------------------------------------------
@@ -2579,15 +2620,8 @@ int sa_compact(const sa_plan *P, const double *vals_dev, int64_t *indptr_out, in
     if (!P) return set_error(SA_ERR_ARG, "plan is NULL");
     SA_TRY(set_device(P->mesh->device));
     cudaStream_t st = (cudaStream_t)stream;
-    const int64_t nr = P->nrows;
-    int64_t *cnt = nullptr;
-    SA_CUDA_TRY(cudaMallocAsync((void **)&cnt, (nr + 1) * sizeof(int64_t), st));
-    if (nr) SA_LAUNCH(k_row_nonzeros, grid_for(nr, 256), 256, 0, st, P->indptr, vals_dev, nr, cnt);
-    SA_TRY(exclusive_scan_i64(cnt, indptr_out, nr, P->scan_tmp, st));
-    if (nr) SA_LAUNCH(k_compact, grid_for(nr, 256), 256, 0, st, P->indptr, P->indices, vals_dev, nr, indptr_out,
-                      indices_out, vals_out);
-    SA_CUDA_TRY(cudaFreeAsync(cnt, st));
-    return SA_OK;
+    return compact_csr(P->indptr, P->indices, vals_dev, P->nrows, P->nnz, P->scan_tmp, indptr_out, indices_out, vals_out,
+                       st);
 }
 
 }  // extern "C"

@@ -289,15 +289,7 @@ int sa_pk_compact(const sa_pk_plan *P, const double *vals_dev, int64_t *indptr_o
     if (!P) return set_error(SA_ERR_ARG, "plan is NULL");
     SA_TRY(set_device(P->device));
     cudaStream_t st = (cudaStream_t)stream;
-    const int64_t nr = P->nq;
-    int64_t *cnt = nullptr;
-    SA_CUDA_TRY(cudaMallocAsync((void **)&cnt, (nr + 1) * sizeof(int64_t), st));
-    if (nr) SA_LAUNCH(k_row_nonzeros, grid_for(nr, 256), 256, 0, st, P->colptr, vals_dev, nr, cnt);
-    SA_TRY(exclusive_scan_i64(cnt, indptr_out, nr, P->scan_tmp, st));
-    if (nr) SA_LAUNCH(k_compact, grid_for(nr, 256), 256, 0, st, P->colptr, P->cols, vals_dev, nr, indptr_out,
-                      indices_out, vals_out);
-    SA_CUDA_TRY(cudaFreeAsync(cnt, st));
-    return SA_OK;
+    return compact_csr(P->colptr, P->cols, vals_dev, P->nq, P->nnz, P->scan_tmp, indptr_out, indices_out, vals_out, st);
 }
 
 }  // extern "C"
