@@ -100,22 +100,38 @@ def _morton_renumber(q, me, n):
     return np.ascontiguousarray(q[:, perm]), np.ascontiguousarray(inv[me])
 
 
-def general_coeffs(cfg, nq):
+_FIELD_CHUNK = 1 << 20
+
+
+def general_coeffs(cfg, nq, lo=0, n=None):
     """C5 nodal fields: A = I + 0.5 R R^T / 3, b, c ~ N(0,1),
-    a0 ~ U[0,1), drawn over the global node numbering."""
-    rng = np.random.default_rng(cfg["seed"])
-    R = rng.standard_normal((nq, 3, 3))
-    # A = I + 0.5 R R^T / 3, built in place (one (nq,3,3) temporary)
-    A = np.einsum("nij,nkj->nik", R, R)
-    del R
-    A *= 0.5
-    A /= 3.0
-    A[:, 0, 0] += 1.0
-    A[:, 1, 1] += 1.0
-    A[:, 2, 2] += 1.0
-    b = rng.standard_normal((nq, 3))
-    c = rng.standard_normal((nq, 3))
-    a0 = rng.uniform(0.0, 1.0, nq)
+    a0 ~ U[0,1) over the global node numbering, nodes [lo, lo + n).  The
+    fields are drawn per chunk of 2^20 nodes from default_rng([seed, chunk]),
+    so a rank draws only the chunks its node window overlaps (at 8 GPUs weak
+    scaling the global fields are 17 GB per process otherwise)."""
+    n = nq - lo if n is None else n
+    A = np.empty((n, 3, 3))
+    b = np.empty((n, 3))
+    c = np.empty((n, 3))
+    a0 = np.empty(n)
+    for j in range(lo // _FIELD_CHUNK, (lo + n + _FIELD_CHUNK - 1) // _FIELD_CHUNK if n else 0):
+        c0 = j * _FIELD_CHUNK
+        cj = min(_FIELD_CHUNK, nq - c0)
+        rng = np.random.default_rng([cfg["seed"], j])
+        R = rng.standard_normal((cj, 3, 3))
+        Aj = np.einsum("nij,nkj->nik", R, R)
+        Aj *= 0.5 / 3.0
+        Aj[:, 0, 0] += 1.0
+        Aj[:, 1, 1] += 1.0
+        Aj[:, 2, 2] += 1.0
+        bj = rng.standard_normal((cj, 3))
+        cjv = rng.standard_normal((cj, 3))
+        a0j = rng.uniform(0.0, 1.0, cj)
+        s0, s1 = max(lo, c0), min(lo + n, c0 + cj)   # global node range of this chunk inside the window
+        A[s0 - lo:s1 - lo] = Aj[s0 - c0:s1 - c0]
+        b[s0 - lo:s1 - lo] = bj[s0 - c0:s1 - c0]
+        c[s0 - lo:s1 - lo] = cjv[s0 - c0:s1 - c0]
+        a0[s0 - lo:s1 - lo] = a0j[s0 - c0:s1 - c0]
     return dict(A=A, b=b, c=c, a0=a0)
 
 
@@ -133,10 +149,10 @@ def make_kernels(cfg, mesh, window=None):
         elif op == "elastic":
             out.append(P.ElasticKernel(mesh, 1.0, 0.5))
         else:
-            nq = mesh.q.shape[1] if window is None else window[1]
-            f = general_coeffs(cfg, nq)
-            if window is not None:
-                f = {k: np.ascontiguousarray(v[window[0]:window[0] + mesh.q.shape[1]]) for k, v in f.items()}
+            if window is None:
+                f = general_coeffs(cfg, mesh.q.shape[1])
+            else:   # the rank's node window of the global fields
+                f = general_coeffs(cfg, window[1], window[0], mesh.q.shape[1])
             out.append(P.GeneralKernel(mesh, exact=os.environ.get("SA_BENCH_EXACT") == "1", **f))
     return out
 

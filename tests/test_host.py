@@ -227,3 +227,19 @@ def test_matrixmarket_writer_matches_reference(tmp_path):
         assert np.array_equal(back.vals, va) and np.array_equal(back.col_idx, ci)
     finally:
         sys.path.remove(ref)
+
+
+def test_bench_fields_windows_are_slices_of_the_global_fields(monkeypatch):
+    # bench.py draws the C5 nodal fields per chunk of nodes, so a rank's
+    # window costs only its chunks: every window is bitwise the slice of the
+    # global draw
+    import bench
+
+    monkeypatch.setattr(bench, "_FIELD_CHUNK", 1000)
+    cfg = {"seed": 14013305}
+    full = bench.general_coeffs(cfg, 3500)
+    assert np.all(np.linalg.eigvalsh(full["A"]) >= 1.0 - 1e-12)   # SPD: I + R R^T / 6
+    for lo, n in [(0, 3500), (0, 10), (990, 20), (1000, 1000), (2999, 501), (3400, 100), (1234, 0)]:
+        w = bench.general_coeffs(cfg, 3500, lo, n)
+        for k in full:
+            assert np.array_equal(w[k], full[k][lo:lo + n]), (k, lo, n)
