@@ -602,7 +602,11 @@ def run_e2e(q, me, vols, kernels, rb, re_, col_offset, nme_global, args, world, 
     pme = torch.from_numpy(me).pin_memory()
     pv = torch.from_numpy(np.asarray(vols)).pin_memory()
     mesh = P.Mesh(pq.numpy(), pme.numpy(), pv.numpy())
-    h2d = pq.numel() * 8 + pme.numel() * 8 + pv.numel() * 8
+    # connectivity: the rows the host narrows cross PCIe as int32 (device.upload_connectivity)
+    from paper_1401_3301_b200.device import connectivity_split
+
+    r32 = connectivity_split(mesh.me, q.shape[0])
+    h2d = pq.numel() * 8 + me.shape[1] * (4 * r32 + 8 * (me.shape[0] - r32)) + pv.numel() * 8
     if all(k.op == "general" and not getattr(k, "exact", False) for k in kernels):
         h2d -= pv.numel() * 8   # fast general operator: volumes recomputed on the device, not uploaded
     # plus the nodal coefficient arrays every assembly uploads (pinned copies
@@ -646,7 +650,8 @@ def run_e2e(q, me, vols, kernels, rb, re_, col_offset, nme_global, args, world, 
             "d2h_bytes_per_step": int(d2h), "ms_per_step": float(t.item()) * 1e3,
             "stages_ms": {k: v / steps for k, v in stages.items()},
             "calls_ms": [round(1e3 * x, 2) for x in times],
-            "path": "assemble_block_b200(Mesh(pinned q, me, vols)): upload -> symbolic -> numeric (pattern "
+            "path": "assemble_block_b200(Mesh(pinned q, me, vols)): upload (connectivity rows narrowed to int32 by the "
+                    "host threads while uploading) -> symbolic -> numeric (pattern "
                     "download overlapped) -> compact -> pinned host CSR (indices cross PCIe as int32, widened to "
                     "int64 on the host while the values transfer)",
             "timing": "host wall clock, median of %d, device synchronized" % len(times)}

@@ -71,6 +71,20 @@ typedef struct sa_plan sa_plan;   /* symbolic phase for one dof-row block       
  * The mesh keeps private device copies (q as padded AoS, me as int32). */
 int sa_mesh_create(int d, int64_t nq, int64_t nme, const double *q_dev, const int64_t *me_dev,
                    const double *vols_dev, int core, int device, void *stream, sa_mesh **out);
+/* Connectivity with its first rows32 rows as int32 ((rows32, nme), narrowed
+ * on the host while uploading: sa_host_narrow_upload) and the remaining
+ * d+1-rows32 rows as int64; otherwise sa_mesh_create. */
+int sa_mesh_create_split(int d, int64_t nq, int64_t nme, const double *q_dev, const int32_t *me32_dev, int rows32,
+                         const int64_t *me_dev, const double *vols_dev, int core, int device, void *stream,
+                         sa_mesh **out);
+/* Host side of the upload: n int64 entries of me (HOST memory) are narrowed
+ * to int32 by nthreads host threads into `staging` (pinned host memory, n
+ * entries), range-checked against [0, nq) in the same pass (first_bad = flat
+ * index a * nme + k of the first bad entry, or -1: the reference's
+ * IndexRangeError, mesh.py:83-87), and copied to dst_dev (device, n entries)
+ * chunk by chunk on `stream` while later chunks are still being narrowed. */
+int sa_host_narrow_upload(const int64_t *src_host, int64_t n, int64_t nq, int32_t *staging_pinned, int32_t *dst_dev,
+                          int nthreads, int device, void *stream, int64_t *first_bad);
 /* q_dev may be NULL in sa_mesh_create: the connectivity is packed and the
  * symbolic phase (which needs only me) can run while the coordinates are
  * still uploading; sa_mesh_set_coords then packs q and copies / computes

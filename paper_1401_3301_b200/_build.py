@@ -16,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIBNAME = "libsimplex_asm_b200.so"
 LIB_PATH = os.path.join(LIBDIR, LIBNAME)
-SOURCES = ["sa_abi.cu", "sa_d1.cu", "sa_d2.cu", "sa_d3.cu", "sa_scan.cu", "sa_meshgen.cu"]
+SOURCES = ["sa_abi.cu", "sa_d1.cu", "sa_d2.cu", "sa_d3.cu", "sa_scan.cu", "sa_meshgen.cu", "sa_host.cu"]
 HEADERS = ["sa_common.cuh", "sa_geometry.cuh", "sa_core.cu", "sa_pk.cuh"]
 
 NVCC_FLAGS = [
@@ -26,6 +26,7 @@ NVCC_FLAGS = [
     # --fmad=false is a second guard against contraction anywhere else
     "--fmad=false",
     "-Xcompiler", "-fPIC",
+    "-Xcompiler", "-pthread",
 ]
 
 
@@ -64,7 +65,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if failed:
         raise RuntimeError(f"nvcc failed for {failed}")
     tmp = LIB_PATH + ".tmp"
-    link = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
+    link = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-pthread", "-o", tmp, *objs]
     if verbose:
         print(" ".join(link), file=sys.stderr)
     subprocess.run(link, check=True)

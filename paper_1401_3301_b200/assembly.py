@@ -16,7 +16,7 @@ import weakref
 import numpy as np
 
 from . import kernels as _k
-from .device import OP_BITS, DeviceCSR, DeviceMesh, upload_coeffs
+from .device import upload_connectivity, OP_BITS, DeviceCSR, DeviceMesh, upload_coeffs
 from .sparse import SparseMatrix
 
 _MESH_CACHE: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
@@ -181,7 +181,10 @@ def assemble_block_b200(mesh, kernels, row_begin: int, row_end: int, core: str =
     # e2e 315 vs 215 ms); coordinates and coefficients follow on a side
     # stream while the symbolic phase runs
     main = torch.cuda.current_stream()
-    med = torch.as_tensor(np.asarray(mesh.me)).to(main.device, non_blocking=True)
+    # connectivity: narrowed to int32 by the host threads while it uploads
+    # (half the PCIe bytes of the reference's int64 array for those rows)
+    nq_ = int(np.asarray(mesh.q).shape[1])
+    me32, med = upload_connectivity(mesh.me, nq_, main.device)
     vols = getattr(mesh, "vols", None)
     # the fast general operator (values within 1e-12, exact pattern) does not
     # need the host volumes bit for bit: they are recomputed on the device
@@ -200,7 +203,7 @@ def assemble_block_b200(mesh, kernels, row_begin: int, row_end: int, core: str =
     # the side stream too, behind the coordinates, during the symbolic phase
     order = sorted(kernels, key=lambda k: OP_BITS[k.op])
     coeffs = upload_coeffs(order, main.device, int(np.asarray(mesh.q).shape[0]), side)
-    dm = DeviceMesh(None, med, vd, core=core, nq=int(np.asarray(mesh.q).shape[1]))
+    dm = DeviceMesh(None, med, vd, core=core, nq=nq_, me32=me32)
     t1 = time.perf_counter()
     plan = dm.plan(kernels[0].m, row_begin, row_end)
     # the kernel-specific plan data (two-pass slot map, element batches) needs

@@ -164,15 +164,17 @@ __global__ void k_pack_q(const double *__restrict__ q, int64_t nq, typename VecT
     }
 }
 
+// (rows [0, rows32) of me may arrive as int32 -- narrowed and range-checked on
+// the host while uploading, sa_host_narrow_upload -- the others as int64)
 template <int D>
-__global__ void k_pack_me(const int64_t *__restrict__ me, int64_t nq, int64_t nme,
-                          typename IdxT<D>::type *__restrict__ out, unsigned long long *bad)
+__global__ void k_pack_me(const int64_t *__restrict__ me, const int32_t *__restrict__ me32, int rows32, int64_t nq,
+                          int64_t nme, typename IdxT<D>::type *__restrict__ out, unsigned long long *bad)
 {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nme; k += (int64_t)gridDim.x * blockDim.x) {
         int v[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int a = 0; a <= D; ++a) {
-            int64_t x = me[a * nme + k];
+            int64_t x = a < rows32 ? (int64_t)me32[a * nme + k] : me[(a - rows32) * nme + k];
             if (x < 0 || x >= nq) atomicMin(bad, (unsigned long long)(a * nme + k));
             v[a] = (int)x;
         }
@@ -1673,7 +1675,8 @@ template <int D>
 int mesh_coords(sa_mesh *M, const double *q, const double *vols, cudaStream_t st);
 
 template <int D>
-int mesh_kernels(sa_mesh *M, const double *q, const int64_t *me, const double *vols, cudaStream_t st)
+int mesh_kernels(sa_mesh *M, const double *q, const int64_t *me, const int32_t *me32, int rows32, const double *vols,
+                 cudaStream_t st)
 {
     typedef typename VecT<D>::type V;
     typedef typename IdxT<D>::type I;
@@ -1683,7 +1686,7 @@ int mesh_kernels(sa_mesh *M, const double *q, const int64_t *me, const double *v
     unsigned gq = std::min<int64_t>(grid_for(M->nq, B), 148 * 32);
     unsigned ge = std::min<int64_t>(grid_for(M->nme, B), 148 * 32);
     if (M->nq && q) SA_LAUNCH(k_pack_q<D>, gq, B, 0, st, q, M->nq, (V *)M->qv);
-    if (M->nme) SA_LAUNCH(k_pack_me<D>, ge, B, 0, st, me, M->nq, M->nme, (I *)M->me, bad);
+    if (M->nme) SA_LAUNCH(k_pack_me<D>, ge, B, 0, st, me, me32, rows32, M->nq, M->nme, (I *)M->me, bad);
     unsigned long long hbad = 0;
     SA_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, st));
     SA_CUDA_TRY(cudaStreamSynchronize(st));
@@ -2163,9 +2166,9 @@ int dispatch_numeric(const sa_plan *P, const NumArgs &a, int ops, int core, cuda
 // these wrappers.
 #define SA_CAT2(a, b) a##b
 #define SA_CAT(a, b) SA_CAT2(a, b)
-int sa_mesh_kernels_d1(sa_mesh *, const double *, const int64_t *, const double *, cudaStream_t);
-int sa_mesh_kernels_d2(sa_mesh *, const double *, const int64_t *, const double *, cudaStream_t);
-int sa_mesh_kernels_d3(sa_mesh *, const double *, const int64_t *, const double *, cudaStream_t);
+int sa_mesh_kernels_d1(sa_mesh *, const double *, const int64_t *, const int32_t *, int, const double *, cudaStream_t);
+int sa_mesh_kernels_d2(sa_mesh *, const double *, const int64_t *, const int32_t *, int, const double *, cudaStream_t);
+int sa_mesh_kernels_d3(sa_mesh *, const double *, const int64_t *, const int32_t *, int, const double *, cudaStream_t);
 int sa_mesh_coords_d1(sa_mesh *, const double *, const double *, cudaStream_t);
 int sa_mesh_coords_d2(sa_mesh *, const double *, const double *, cudaStream_t);
 int sa_mesh_coords_d3(sa_mesh *, const double *, const double *, cudaStream_t);
@@ -2187,9 +2190,10 @@ int SA_CAT(sa_mesh_revols_d, SA_D)(const sa_mesh *M, double *out, cudaStream_t s
 #if SA_D == 3
 int sa_winc_d3(sa_plan *P, cudaStream_t st) { return build_winc<3>(P, st); }
 #endif
-int SA_CAT(sa_mesh_kernels_d, SA_D)(sa_mesh *M, const double *q, const int64_t *me, const double *vols, cudaStream_t st)
+int SA_CAT(sa_mesh_kernels_d, SA_D)(sa_mesh *M, const double *q, const int64_t *me, const int32_t *me32, int rows32,
+                                    const double *vols, cudaStream_t st)
 {
-    return mesh_kernels<SA_D>(M, q, me, vols, st);
+    return mesh_kernels<SA_D>(M, q, me, me32, rows32, vols, st);
 }
 int SA_CAT(sa_symbolic_d, SA_D)(sa_plan *P, cudaStream_t st) { return symbolic_kernels<SA_D>(P, st); }
 int SA_CAT(sa_mesh_coords_d, SA_D)(sa_mesh *M, const double *q, const double *vols, cudaStream_t st)
@@ -2239,14 +2243,17 @@ int64_t sa_launch_count(int reset)
     return v;
 }
 
-int sa_mesh_create(int d, int64_t nq, int64_t nme, const double *q_dev, const int64_t *me_dev,
-                   const double *vols_dev, int core, int device, void *stream, sa_mesh **out)
+int sa_mesh_create_split(int d, int64_t nq, int64_t nme, const double *q_dev, const int32_t *me32_dev, int rows32,
+                         const int64_t *me_dev, const double *vols_dev, int core, int device, void *stream,
+                         sa_mesh **out)
 {
     err_state().msg.clear();
     err_state().bad = -1;
     if (!out) return set_error(SA_ERR_ARG, "out is NULL");
     *out = nullptr;
     if (d < 1 || d > 3) return set_error(SA_ERR_ARG, "dimension must be 1, 2 or 3, got %d", d);
+    if (rows32 < 0 || rows32 > d + 1 || (rows32 > 0 && !me32_dev && nme) || (rows32 <= d && !me_dev && nme))
+        return set_error(SA_ERR_ARG, "connectivity: %d int32 rows of %d, missing array", rows32, d + 1);
     if (core != CORE_SKYLAKEX && core != CORE_HASWELL) return set_error(SA_ERR_ARG, "unknown core %d", core);
     if (nq < 0 || nme < 0) return set_error(SA_ERR_ARG, "negative sizes");
     if (nq >= ((int64_t)1 << 31) || nme >= ((int64_t)1 << 30))
@@ -2266,12 +2273,18 @@ int sa_mesh_create(int d, int64_t nq, int64_t nme, const double *q_dev, const in
         cudaMallocAsync((void **)&M->vols, std::max<int64_t>(nme, 1) * sizeof(double), st) != cudaSuccess ||
         cudaMallocAsync((void **)&M->scratch, 8 * sizeof(int64_t), st) != cudaSuccess)
         return fail(set_error(SA_ERR_NOMEM, "device allocation for the mesh failed"));
-    if (d == 1) rc = sa_mesh_kernels_d1(M, q_dev, me_dev, vols_dev, st);
-    else if (d == 2) rc = sa_mesh_kernels_d2(M, q_dev, me_dev, vols_dev, st);
-    else rc = sa_mesh_kernels_d3(M, q_dev, me_dev, vols_dev, st);
+    if (d == 1) rc = sa_mesh_kernels_d1(M, q_dev, me_dev, me32_dev, rows32, vols_dev, st);
+    else if (d == 2) rc = sa_mesh_kernels_d2(M, q_dev, me_dev, me32_dev, rows32, vols_dev, st);
+    else rc = sa_mesh_kernels_d3(M, q_dev, me_dev, me32_dev, rows32, vols_dev, st);
     if (rc != SA_OK) return fail(rc);
     *out = M;
     return SA_OK;
+}
+
+int sa_mesh_create(int d, int64_t nq, int64_t nme, const double *q_dev, const int64_t *me_dev,
+                   const double *vols_dev, int core, int device, void *stream, sa_mesh **out)
+{
+    return sa_mesh_create_split(d, nq, nme, q_dev, nullptr, 0, me_dev, vols_dev, core, device, stream, out);
 }
 
 int sa_mesh_set_coords(sa_mesh *M, const double *q_dev, const double *vols_dev, void *stream)

@@ -53,7 +53,8 @@ class DeviceMesh:
     layout) or CUDA tensors.  ``vols=None`` computes volumes on the device.
     """
 
-    def __init__(self, q, me, vols=None, *, core: str = "SkylakeX", device=None, stream=None, nq: int | None = None):
+    def __init__(self, q, me, vols=None, *, core: str = "SkylakeX", device=None, stream=None, nq: int | None = None,
+                 me32=None):
         dev = _require_cuda(device)
         L = _lib.load()
         self.device = dev
@@ -62,16 +63,26 @@ class DeviceMesh:
             # q=None (with nq): connectivity only; set_coords() later -- the
             # symbolic phase can run while the coordinates upload
             qd = _to_dev(q, torch.float64, dev) if q is not None else None
-            med = _to_dev(me, torch.int64, dev)
+            # me32: the first rows of the connectivity already on the device
+            # as int32 (upload_connectivity); ``me`` then holds the remaining
+            # int64 rows (or None)
+            med = _to_dev(me, torch.int64, dev) if me is not None else None
+            rows32 = int(me32.shape[0]) if me32 is not None else 0
+            rows = rows32 + (int(med.shape[0]) if med is not None and med.dim() == 2 else 0)
             vd = _to_dev(vols, torch.float64, dev) if vols is not None else None
-            self.d = int(med.shape[0]) - 1 if qd is None else int(qd.shape[0])
+            self.d = rows - 1 if qd is None else int(qd.shape[0])
             self.nq = int(nq) if qd is None else int(qd.shape[1])
-            self.nme = int(med.shape[1]) if med.dim() == 2 else 0
-            if med.shape[0] != self.d + 1:
-                raise ValueError(f"connectivity shape {tuple(med.shape)} does not match ({self.d + 1}, nme)")
+            some = me32 if me32 is not None else med
+            self.nme = int(some.shape[1]) if some is not None and some.dim() == 2 else 0
+            if rows != self.d + 1:
+                raise ValueError(f"connectivity with {rows} rows does not match ({self.d + 1}, nme)")
             h = ctypes.c_void_p()
-            rc = L.sa_mesh_create(self.d, self.nq, self.nme, _ptr(qd), _ptr(med), _ptr(vd), _lib.SA_CORE[core],
-                                  dev.index, _stream_ptr(stream), ctypes.byref(h))
+            if me32 is not None:
+                rc = L.sa_mesh_create_split(self.d, self.nq, self.nme, _ptr(qd), _ptr(me32), rows32, _ptr(med), _ptr(vd),
+                                            _lib.SA_CORE[core], dev.index, _stream_ptr(stream), ctypes.byref(h))
+            else:
+                rc = L.sa_mesh_create(self.d, self.nq, self.nme, _ptr(qd), _ptr(med), _ptr(vd), _lib.SA_CORE[core],
+                                      dev.index, _stream_ptr(stream), ctypes.byref(h))
             _lib.check(rc)
         self._h = h
         self._plans = {}
@@ -339,6 +350,83 @@ def upload_coeffs(kernels, device, d, stream=None) -> tuple[_lib.SaCoeffs, list]
         elif k.op == "general":
             c.gen_packed = up(k, "packed", k.packed())
     return c, keep
+
+
+# page-locked int32 staging buffer of upload_connectivity: grow-only and
+# reused across calls (a fresh pinned allocation per call costs more than
+# the upload it serves)
+_STAGING: dict = {}
+
+
+def _staging_buffer(n: int) -> "torch.Tensor":
+    ev = _STAGING.get("event")
+    if ev is not None:
+        ev.synchronize()
+    buf = _STAGING.get("buf")
+    if buf is None or buf.numel() < n:
+        _STAGING["buf"] = None
+        buf = torch.empty(max(n, 1), dtype=torch.int32, pin_memory=True)
+        _STAGING["buf"] = buf
+    return buf[:n]
+
+
+def connectivity_split(me, d: int) -> int:
+    """How many leading rows of a host connectivity array upload_connectivity
+    narrows to int32 on the host (the others cross PCIe as int64): all but
+    the last when the array is page-locked (the int64 row's DMA keeps PCIe
+    busy while the host threads narrow), every row otherwise, 0 when the
+    array cannot be narrowed in place (not int64 / not C-contiguous)."""
+    a = np.asarray(me)
+    if a.dtype != np.int64 or a.ndim != 2 or not a.flags.c_contiguous or a.shape[1] == 0:
+        return 0
+    import warnings
+
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")   # read-only arrays (frozen meshes)
+        pinned = torch.cuda.is_available() and torch.from_numpy(a).is_pinned()
+    return d if (pinned and d >= 1) else d + 1
+
+
+def upload_connectivity(me, nq: int, device, stream=None):
+    """Host (d+1, nme) int64 connectivity -> (me32 device (rows32, nme) int32,
+    me64 device (d+1-rows32, nme) int64 or None).  The host threads narrow
+    and range-check the first rows (sa_host_narrow_upload) while the copies
+    run; raises IndexRangeError naming me[a, k] like the reference."""
+    import os
+
+    from .errors import IndexRangeError
+
+    a = np.asarray(me)
+    d = a.shape[0] - 1
+    rows32 = connectivity_split(a, d)
+    if rows32 == 0:
+        return None, _to_dev(a, torch.int64, device)
+    nme = a.shape[1]
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    with torch.cuda.device(device), torch.cuda.stream(s):
+        import warnings
+
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            me64 = torch.from_numpy(a[rows32:]).to(device, non_blocking=True) if rows32 <= d else None
+        staging = _staging_buffer(rows32 * nme).view(rows32, nme)
+        me32 = torch.empty((rows32, nme), dtype=torch.int32, device=device)
+        bad = ctypes.c_int64(-1)
+        try:
+            nthreads = len(os.sched_getaffinity(0))
+        except AttributeError:  # pragma: no cover
+            nthreads = os.cpu_count() or 1
+        rc = _lib.load().sa_host_narrow_upload(ctypes.c_void_p(a.ctypes.data), rows32 * nme, int(nq),
+                                               _ptr(staging), _ptr(me32), nthreads, device.index,
+                                               ctypes.c_void_p(s.cuda_stream), ctypes.byref(bad))
+        _lib.check(rc)
+        ev = torch.cuda.Event()
+        ev.record(s)
+    if bad.value >= 0:
+        ev.synchronize()
+        raise IndexRangeError(f"connectivity entry me[{bad.value // nme}, {bad.value % nme}] out of range [0, {nq})")
+    _STAGING["event"] = ev   # the next upload waits for these copies before reusing the buffer
+    return me32, me64
 
 
 def device_volumes(q, me, core: str = "SkylakeX") -> np.ndarray:

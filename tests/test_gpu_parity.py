@@ -747,3 +747,35 @@ def test_mesh_validate_on_device(cuda_ok):
     v = mesh.vols.copy()
     v[9] *= 1.0 + 2e-13    # inside the tolerance
     P.Mesh(mesh.q, mesh.me, v).validate()
+
+
+def test_block_upload_narrows_connectivity_on_the_host(cuda_ok):
+    # assemble_block_b200 narrows the int64 connectivity to int32 on the host
+    # while uploading (sa_host_narrow_upload): same matrices from pageable,
+    # page-locked, read-only and non-contiguous arrays; a bad index -- also
+    # one whose low 32 bits look valid -- raises the reference's IndexRangeError
+    import torch
+
+    from paper_1401_3301_b200.assembly import assemble_block_b200
+    from paper_1401_3301_b200.device import connectivity_split
+    from paper_1401_3301_b200.errors import IndexRangeError
+
+    mesh = _jittered(3, 9, 21)
+    nq = mesh.q.shape[1]
+    k = P.StiffnessKernel(mesh)
+    want = P.assemble_b200(mesh, k)
+    pinned = torch.from_numpy(mesh.me.copy()).pin_memory().numpy()
+    ro = mesh.me.copy()
+    ro.setflags(write=False)
+    fortran = np.asfortranarray(mesh.me)
+    assert connectivity_split(pinned, 3) == 3 and connectivity_split(mesh.me.copy(), 3) == 4
+    assert connectivity_split(fortran, 3) == 0 and connectivity_split(mesh.me.astype(np.int32), 3) == 0
+    for me in (mesh.me.copy(), pinned, ro, fortran):
+        (b,) = assemble_block_b200(P.Mesh(mesh.q, me, mesh.vols), [k], 0, nq)
+        assert_csr_equal(b, want.row_ptr, want.col_idx, want.vals)
+    for bad_val in (nq, -1, (1 << 32) + 5):
+        for src in (mesh.me.copy(), pinned.copy()):
+            src[1, 77] = bad_val
+            src[3, 5] = -7
+            with pytest.raises(IndexRangeError, match=rf"me\[1, 77\] out of range \[0, {nq}\)"):
+                assemble_block_b200(P.Mesh(mesh.q, src, mesh.vols), [k], 0, nq)
