@@ -85,6 +85,10 @@ int sa_mesh_create_split(int d, int64_t nq, int64_t nme, const double *q_dev, co
  * chunk by chunk on `stream` while later chunks are still being narrowed. */
 int sa_host_narrow_upload(const int64_t *src_host, int64_t n, int64_t nq, int32_t *staging_pinned, int32_t *dst_dev,
                           int nthreads, int device, void *stream, int64_t *first_bad);
+/* dst[i] = (int64) src[i] + offset on the same host thread pool: the int32
+ * column indices that crossed PCIe, widened to the reference's int64
+ * (sparse.py:53-55); offset shifts a slab's columns to global dofs. */
+int sa_host_widen_i32(const int32_t *src_host, int64_t n, int64_t offset, int64_t *dst_host, int nthreads);
 /* q_dev may be NULL in sa_mesh_create: the connectivity is packed and the
  * symbolic phase (which needs only me) can run while the coordinates are
  * still uploading; sa_mesh_set_coords then packs q and copies / computes

@@ -24,7 +24,7 @@ SA_CORE = {"SkylakeX": 0, "Haswell": 1}
 
 # every symbol include/simplex_asm_b200.h declares
 EXPORTS = (
-    "sa_mesh_create", "sa_mesh_create_split", "sa_host_narrow_upload", "sa_mesh_vols", "sa_mesh_validate",
+    "sa_mesh_create", "sa_mesh_create_split", "sa_host_narrow_upload", "sa_host_widen_i32", "sa_mesh_vols", "sa_mesh_validate",
     "sa_mesh_destroy",
     "sa_plan_create", "sa_plan_info", "sa_plan_stats", "sa_plan_pattern", "sa_plan_destroy",
     "sa_numeric", "sa_compact", "sa_plan_prepare", "sa_mesh_set_coords", "sa_kuhn_mesh", "sa_kuhn_slab",
@@ -77,6 +77,7 @@ def load(build_if_missing: bool = True):
     L.sa_mesh_create_split.argtypes = [ctypes.c_int, i64, i64, vp, vp, ctypes.c_int, vp, vp, ctypes.c_int, ctypes.c_int,
                                        vp, ctypes.POINTER(vp)]
     L.sa_host_narrow_upload.argtypes = [vp, i64, i64, vp, vp, ctypes.c_int, ctypes.c_int, vp, i64p]
+    L.sa_host_widen_i32.argtypes = [vp, i64, i64, vp, ctypes.c_int]
     L.sa_mesh_vols.argtypes = [vp, vp, vp]
     L.sa_mesh_validate.argtypes = [vp, vp, i64p, i64p, vp]
     L.sa_mesh_destroy.argtypes = [vp]

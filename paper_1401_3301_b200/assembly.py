@@ -11,6 +11,7 @@ so ``simplex_asm.bench`` and its CLI dispatch to the B200 as variant "b200".
 
 from __future__ import annotations
 
+import ctypes
 import weakref
 
 import numpy as np
@@ -102,9 +103,14 @@ class _PatternDownload:
         if self._host is None:
             self.done.synchronize()
             ix64 = torch.empty(self.ix32.shape, dtype=torch.int64, pin_memory=True)
-            ix64.copy_(self.ix32)
-            if self.host_offset:
-                ix64 += self.host_offset
+            # widened on the library's own parked host threads (a torch CPU op
+            # would leave its OpenMP workers spinning into the next upload)
+            from . import _lib
+            from .device import _host_threads
+
+            _lib.check(_lib.load().sa_host_widen_i32(ctypes.c_void_p(self.ix32.data_ptr()), self.ix32.numel(),
+                                                     int(self.host_offset), ctypes.c_void_p(ix64.data_ptr()),
+                                                     _host_threads()))
             self._host = (self.ip.numpy(), ix64.numpy())
         return self._host
 

@@ -370,6 +370,25 @@ def _staging_buffer(n: int) -> "torch.Tensor":
     return buf[:n]
 
 
+def _host_threads() -> int:
+    """Host threads for the narrowing pass: the CPUs this process may run on
+    (affinity mask, capped by a cgroup CPU quota when one is set)."""
+    import os
+
+    try:
+        n = len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        n = os.cpu_count() or 1
+    try:
+        with open("/sys/fs/cgroup/cpu.max") as f:
+            quota, period = f.read().split()[:2]
+        if quota != "max":
+            n = max(1, min(n, int(int(quota) / int(period))))
+    except Exception:
+        pass
+    return int(os.environ.get("SA_UPLOAD_THREADS", n))
+
+
 def connectivity_split(me, d: int) -> int:
     """How many leading rows of a host connectivity array upload_connectivity
     narrows to int32 on the host (the others cross PCIe as int64): all but
@@ -412,10 +431,7 @@ def upload_connectivity(me, nq: int, device, stream=None):
         staging = _staging_buffer(rows32 * nme).view(rows32, nme)
         me32 = torch.empty((rows32, nme), dtype=torch.int32, device=device)
         bad = ctypes.c_int64(-1)
-        try:
-            nthreads = len(os.sched_getaffinity(0))
-        except AttributeError:  # pragma: no cover
-            nthreads = os.cpu_count() or 1
+        nthreads = _host_threads()
         rc = _lib.load().sa_host_narrow_upload(ctypes.c_void_p(a.ctypes.data), rows32 * nme, int(nq),
                                                _ptr(staging), _ptr(me32), nthreads, device.index,
                                                ctypes.c_void_p(s.cuda_stream), ctypes.byref(bad))
