@@ -356,6 +356,7 @@ def upload_coeffs(kernels, device, d, stream=None) -> tuple[_lib.SaCoeffs, list]
 # reused across calls (a fresh pinned allocation per call costs more than
 # the upload it serves)
 _STAGING: dict = {}
+_NARROW_MIN_ENTRIES = 48 << 20
 
 
 def _staging_buffer(n: int) -> "torch.Tensor":
@@ -397,6 +398,10 @@ def connectivity_split(me, d: int) -> int:
     array cannot be narrowed in place (not int64 / not C-contiguous)."""
     a = np.asarray(me)
     if a.dtype != np.int64 or a.ndim != 2 or not a.flags.c_contiguous or a.shape[1] == 0:
+        return 0
+    # small arrays: waking the host threads costs more than the PCIe bytes
+    # saved (measured: C2, 24 M entries, 20.1 vs 18.6 ms end to end)
+    if a.size < _NARROW_MIN_ENTRIES:
         return 0
     import warnings
 

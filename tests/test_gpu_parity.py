@@ -749,7 +749,7 @@ def test_mesh_validate_on_device(cuda_ok):
     P.Mesh(mesh.q, mesh.me, v).validate()
 
 
-def test_block_upload_narrows_connectivity_on_the_host(cuda_ok):
+def test_block_upload_narrows_connectivity_on_the_host(cuda_ok, monkeypatch):
     # assemble_block_b200 narrows the int64 connectivity to int32 on the host
     # while uploading (sa_host_narrow_upload): same matrices from pageable,
     # page-locked, read-only and non-contiguous arrays; a bad index -- also
@@ -760,6 +760,9 @@ def test_block_upload_narrows_connectivity_on_the_host(cuda_ok):
     from paper_1401_3301_b200.device import connectivity_split
     from paper_1401_3301_b200.errors import IndexRangeError
 
+    from paper_1401_3301_b200 import device as D
+
+    monkeypatch.setattr(D, "_NARROW_MIN_ENTRIES", 0)   # (small arrays normally upload as they are)
     mesh = _jittered(3, 9, 21)
     nq = mesh.q.shape[1]
     k = P.StiffnessKernel(mesh)
