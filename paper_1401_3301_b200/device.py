@@ -356,6 +356,7 @@ def upload_coeffs(kernels, device, d, stream=None) -> tuple[_lib.SaCoeffs, list]
 # reused across calls (a fresh pinned allocation per call costs more than
 # the upload it serves)
 _STAGING: dict = {}
+_STAGING_LOCK = __import__("threading").Lock()   # one upload at a time fills the buffer
 _NARROW_MIN_ENTRIES = 48 << 20
 
 
@@ -416,8 +417,6 @@ def upload_connectivity(me, nq: int, device, stream=None):
     me64 device (d+1-rows32, nme) int64 or None).  The host threads narrow
     and range-check the first rows (sa_host_narrow_upload) while the copies
     run; raises IndexRangeError naming me[a, k] like the reference."""
-    import os
-
     from .errors import IndexRangeError
 
     a = np.asarray(me)
@@ -427,7 +426,7 @@ def upload_connectivity(me, nq: int, device, stream=None):
         return None, _to_dev(a, torch.int64, device)
     nme = a.shape[1]
     s = stream if stream is not None else torch.cuda.current_stream(device)
-    with torch.cuda.device(device), torch.cuda.stream(s):
+    with _STAGING_LOCK, torch.cuda.device(device), torch.cuda.stream(s):
         import warnings
 
         with warnings.catch_warnings():
@@ -443,10 +442,10 @@ def upload_connectivity(me, nq: int, device, stream=None):
         _lib.check(rc)
         ev = torch.cuda.Event()
         ev.record(s)
+        _STAGING["event"] = ev   # the next upload waits for these copies before reusing the buffer
     if bad.value >= 0:
         ev.synchronize()
         raise IndexRangeError(f"connectivity entry me[{bad.value // nme}, {bad.value % nme}] out of range [0, {nq})")
-    _STAGING["event"] = ev   # the next upload waits for these copies before reusing the buffer
     return me32, me64
 
 
