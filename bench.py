@@ -617,7 +617,7 @@ def run_e2e(q, me, vols, kernels, rb, re_, col_offset, nme_global, args, world, 
             if isinstance(v, np.ndarray):
                 h2d += v.nbytes
         if k.op == "general":
-            h2d += k.packed().nbytes
+            h2d += k.packed_columns()[0].nbytes   # the varying, distinct coefficient columns
     # two untimed calls (pinned staging buffers and pool memory are set up on
     # first use), then the median of up to 7 timed calls
     steps = max(3, min(args.steps, 7))

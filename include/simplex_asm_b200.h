@@ -128,6 +128,14 @@ int sa_plan_pattern(const sa_plan *plan, int64_t *indptr_dev, int32_t *indices_d
 int sa_plan_stats(const sa_plan *plan, int64_t *out, int n);
 int sa_plan_destroy(sa_plan *plan);
 
+/* General-operator coefficient records (nq, 16) = [A 3x3 | b | c | a0] from a
+ * column-compacted upload (nq, nv): record column j is uploaded column
+ * colmap16[j], or the constant consts16[j] when colmap16[j] < 0.  Columns that
+ * are constant over the nodes or repeat another column (a symmetric A) stay
+ * on the host.  colmap16 / consts16 are HOST arrays of 16 entries. */
+int sa_unpack_columns(const double *src_dev, int nv, const int32_t *colmap16_host, const double *consts16_host,
+                      int64_t nq, double *dst_dev, void *stream);
+
 /* ---- numeric phase (repeated for new coefficients) --------------------- */
 
 /* Nodal coefficients (device pointers, nq entries unless stated) or

@@ -27,7 +27,7 @@ EXPORTS = (
     "sa_mesh_create", "sa_mesh_create_split", "sa_host_narrow_upload", "sa_host_widen_i32", "sa_mesh_vols", "sa_mesh_validate",
     "sa_mesh_destroy",
     "sa_plan_create", "sa_plan_info", "sa_plan_stats", "sa_plan_pattern", "sa_plan_destroy",
-    "sa_numeric", "sa_compact", "sa_plan_prepare", "sa_mesh_set_coords", "sa_kuhn_mesh", "sa_kuhn_slab",
+    "sa_numeric", "sa_compact", "sa_unpack_columns", "sa_plan_prepare", "sa_mesh_set_coords", "sa_kuhn_mesh", "sa_kuhn_slab",
     "sa_pk_plan_create", "sa_pk_plan_info", "sa_pk_plan_pattern", "sa_pk_mass", "sa_pk_compact", "sa_pk_plan_destroy",
     "sa_last_error", "sa_bad_index", "sa_launch_count",
 )
@@ -88,6 +88,7 @@ def load(build_if_missing: bool = True):
     L.sa_plan_destroy.argtypes = [vp]
     L.sa_numeric.argtypes = [vp, ctypes.c_int, ctypes.POINTER(SaCoeffs), ctypes.POINTER(vp), i64p, vp]
     L.sa_plan_prepare.argtypes = [vp, ctypes.c_int, vp]
+    L.sa_unpack_columns.argtypes = [vp, ctypes.c_int, vp, vp, i64, vp, vp]
     L.sa_mesh_set_coords.argtypes = [vp, vp, vp, vp]
     L.sa_pk_plan_create.argtypes = [ctypes.c_int, i64, i64, vp, ctypes.c_int, vp, ctypes.POINTER(vp)]
     L.sa_pk_plan_info.argtypes = [vp, i64p, i64p]

@@ -1650,6 +1650,24 @@ __global__ void k_compact(const int64_t *__restrict__ indptr, const int32_t *__r
     }
 }
 
+// general-operator coefficient records from their column-compacted upload:
+// column j of the 16-double record is column map[j] of the nv uploaded ones,
+// or the constant cst[j] when map[j] < 0 (columns that are constant over the
+// nodes, or equal to another column -- a symmetric A -- do not cross PCIe)
+struct UnpackCols {
+    int map[16];
+    double cst[16];
+};
+__global__ void k_unpack_columns(const double *__restrict__ src, int nv, UnpackCols u, int64_t nq, double *__restrict__ dst)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq * 16; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t node = i >> 4;
+        const int j = (int)(i & 15);
+        const int m = u.map[j];
+        dst[i] = m >= 0 ? src[node * nv + m] : u.cst[j];
+    }
+}
+
 // canonical CSR from a structural one (shared by sa_compact / sa_pk_compact)
 inline int compact_csr(const int64_t *indptr, const int32_t *indices, const double *vals, int64_t nr, int64_t nnz,
                        int64_t *scan_tmp, int64_t *indptr_out, int32_t *indices_out, double *vals_out, cudaStream_t st)
@@ -2624,6 +2642,23 @@ int sa_numeric(sa_plan *P, int ops, const sa_coeffs *cf, double *const *vals_dev
             return set_error(SA_ERR_DEGENERATE, "simplex %lld is degenerate (zero volume)", (long long)h[4]);
         }
     }
+    return SA_OK;
+}
+
+int sa_unpack_columns(const double *src_dev, int nv, const int32_t *colmap16_host, const double *consts16_host, int64_t nq,
+                      double *dst_dev, void *stream)
+{
+    if (!dst_dev || !colmap16_host || !consts16_host || nv < 0 || nv > 16 || (nv > 0 && !src_dev))
+        return set_error(SA_ERR_ARG, "sa_unpack_columns: bad argument");
+    UnpackCols u;
+    for (int j = 0; j < 16; ++j) {
+        if (colmap16_host[j] >= nv) return set_error(SA_ERR_ARG, "sa_unpack_columns: column map entry out of range");
+        u.map[j] = colmap16_host[j];
+        u.cst[j] = consts16_host[j];
+    }
+    if (nq > 0)
+        SA_LAUNCH(k_unpack_columns, std::min<int64_t>(grid_for(nq * 16, 256), 148 * 32), 256, 0, (cudaStream_t)stream,
+                  src_dev, nv, u, nq, dst_dev);
     return SA_OK;
 }
 

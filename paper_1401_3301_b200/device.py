@@ -348,7 +348,22 @@ def upload_coeffs(kernels, device, d, stream=None) -> tuple[_lib.SaCoeffs, list]
             else:
                 c.mu_const = k.mu_const
         elif k.op == "general":
-            c.gen_packed = up(k, "packed", k.packed())
+            # only the varying, distinct columns of the records cross PCIe
+            # (C5: 13 of 16 -- A is symmetric); rebuilt on the device
+            cols, colmap, consts = k.packed_columns()
+            nq = int(cols.shape[0])
+            with torch.cuda.stream(s):
+                rec = torch.empty((nq, 16), dtype=torch.float64, device=device)
+                src = _pinned(k, "cols", cols).to(device=device, non_blocking=True) if cols.shape[1] else None
+                cm = np.ascontiguousarray(colmap, dtype=np.int32)
+                cs = np.ascontiguousarray(consts, dtype=np.float64)
+                with torch.cuda.device(device):
+                    _lib.check(_lib.load().sa_unpack_columns(_ptr(src), int(cols.shape[1]), ctypes.c_void_p(cm.ctypes.data),
+                                                             ctypes.c_void_p(cs.ctypes.data), nq, _ptr(rec),
+                                                             ctypes.c_void_p(s.cuda_stream)))
+            keep.append(rec)
+            keep.append(src)
+            c.gen_packed = _ptr(rec)
     return c, keep
 
 

@@ -157,6 +157,7 @@ class GeneralKernel:
         # both modes (guarded rows are recomputed in reference order).
         self.exact = bool(exact)
         self._packed = None
+        self._cols = None
 
     def packed(self) -> np.ndarray:
         """Nodal coefficients as one 128-byte record per node,
@@ -177,6 +178,33 @@ class GeneralKernel:
             self._packed = p
         return self._packed
 
+    def packed_columns(self):
+        """(cols (nq, nv) f64, colmap (16,) int32, consts (16,) f64): the
+        record of ``packed()`` with the columns that are constant over the
+        nodes (zero padding, absent terms, constant fields) or repeat an
+        earlier column (a symmetric A) left out -- what crosses PCIe;
+        ``sa_unpack_columns`` rebuilds the 128-byte records on the device,
+        bit for bit.  Computed once per coefficient set."""
+        if getattr(self, "_cols", None) is None:
+            p = self.packed()
+            colmap = np.full(16, -1, dtype=np.int32)
+            consts = np.zeros(16)
+            keep = []
+            mirror = {3: 1, 6: 2, 7: 5}   # A[1][0] ~ A[0][1], A[2][0] ~ A[0][2], A[2][1] ~ A[1][2]
+            for j in range(16):
+                col = p[:, j]
+                if col.size == 0 or np.all(col == col[0]):
+                    consts[j] = col[0] if col.size else 0.0
+                    continue
+                k = mirror.get(j)
+                if k is not None and colmap[k] >= 0 and np.array_equal(col, p[:, k]):
+                    colmap[j] = colmap[k]
+                    continue
+                colmap[j] = len(keep)
+                keep.append(j)
+            self._cols = (np.ascontiguousarray(p[:, keep]), colmap, consts)
+        return self._cols
+
 
 def restrict(kernel, mesh_local, nodes: slice, elements):
     """The descriptor ``kernel`` on a sub-mesh (a rank's slab,
@@ -189,6 +217,7 @@ def restrict(kernel, mesh_local, nodes: slice, elements):
     k.mesh = mesh_local
     k.__dict__.pop("_pinned_cache", None)
     k.__dict__.pop("_packed", None)
+    k.__dict__.pop("_cols", None)
     for name in ("w", "lamb", "mu", "A", "b", "c", "a0"):
         v = getattr(kernel, name, None)
         if isinstance(v, np.ndarray) and v.ndim >= 1 and v.shape[0] == kernel.mesh.q.shape[1]:

@@ -243,3 +243,30 @@ def test_bench_fields_windows_are_slices_of_the_global_fields(monkeypatch):
         w = bench.general_coeffs(cfg, 3500, lo, n)
         for k in full:
             assert np.array_equal(w[k], full[k][lo:lo + n]), (k, lo, n)
+
+
+def test_general_kernel_column_compaction_roundtrip():
+    # packed_columns(): constant / repeated columns of the 16-double records
+    # stay on the host; expanding with the column map gives packed() back
+    import paper_1401_3301_b200 as P
+
+    rng = np.random.default_rng(0)
+    q, me = P.hypercube_arrays(3, 3)
+    mesh = P.Mesh(q, me, np.ones(me.shape[1]))
+    nq = q.shape[1]
+    R = rng.standard_normal((nq, 3, 3))
+    sym = np.eye(3)[None] + np.einsum("nij,nkj->nik", R, R)
+    cases = [
+        (dict(A=sym, b=rng.standard_normal((nq, 3)), c=rng.standard_normal((nq, 3)), a0=rng.uniform(0, 1, nq)), 13),
+        (dict(A=R, b=rng.standard_normal((nq, 3))), 12),
+        (dict(A=np.eye(3)), 0),
+        (dict(A=sym, c=np.array([1.0, 0.0, 2.0]), a0=3.0), 6),
+    ]
+    for kw, nv in cases:
+        k = P.GeneralKernel(mesh, **kw)
+        cols, colmap, consts = k.packed_columns()
+        assert cols.shape == (nq, nv) and cols.flags.c_contiguous
+        full = np.empty((nq, 16))
+        for j in range(16):
+            full[:, j] = cols[:, colmap[j]] if colmap[j] >= 0 else consts[j]
+        assert np.array_equal(full, k.packed())
