@@ -403,6 +403,11 @@ def _host_threads() -> int:
             n = max(1, min(n, int(int(quota) / int(period))))
     except Exception:
         pass
+    # several ranks on one host (torchrun): share the CPUs
+    try:
+        n = max(1, n // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1"))))
+    except ValueError:
+        pass
     return int(os.environ.get("SA_UPLOAD_THREADS", n))
 
 
