@@ -50,6 +50,16 @@ int set_error(int status, const char *fmt, ...);
 int tune_int(const char *key, int dflt);
 bool tune_is(const char *key, const char *value);
 
+// Small device->host read-backs (sizes, counters, flags) that do not go
+// through the copy engines: a one-warp kernel writes the words into mapped
+// pinned host memory, and sync_stream() -- cudaStreamSynchronize plus the
+// delivery of this thread's pending read-backs -- hands them over.  A
+// cudaMemcpyAsync of 8 bytes queues behind every device->host copy submitted
+// before it on ANY stream (measured: the library's plan construction stalled
+// 20 ms behind a 1 GB pattern download running on another stream).
+int readback(void *host_dst, const void *dev_src, size_t bytes, cudaStream_t st);
+int sync_stream(cudaStream_t st);
+
 inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
 
 // Device-wide exclusive scan of int64 (in place allowed): out[i] = sum_{j<i} in[j],

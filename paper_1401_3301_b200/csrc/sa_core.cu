@@ -1706,8 +1706,8 @@ int mesh_kernels(sa_mesh *M, const double *q, const int64_t *me, const int32_t *
     if (M->nq && q) SA_LAUNCH(k_pack_q<D>, gq, B, 0, st, q, M->nq, (V *)M->qv);
     if (M->nme) SA_LAUNCH(k_pack_me<D>, ge, B, 0, st, me, me32, rows32, M->nq, M->nme, (I *)M->me, bad);
     unsigned long long hbad = 0;
-    SA_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, st));
-    SA_CUDA_TRY(cudaStreamSynchronize(st));
+    SA_TRY(readback(&hbad, bad, sizeof hbad, st));
+    SA_TRY(sync_stream(st));
     if (hbad != ~0ull) {
         err_state().bad = (int64_t)hbad;
         return set_error(SA_ERR_INDEX_RANGE, "connectivity entry me[%lld, %lld] out of range [0, %lld)",
@@ -1746,8 +1746,8 @@ int mesh_coords(sa_mesh *M, const double *q, const double *vols, cudaStream_t st
             SA_LAUNCH((k_volumes<D, CORE_SKYLAKEX>), ge, B, 0, st, (const V *)M->qv, (const I *)M->me, M->nme, M->vols, bad);
         else
             SA_LAUNCH((k_volumes<D, CORE_HASWELL>), ge, B, 0, st, (const V *)M->qv, (const I *)M->me, M->nme, M->vols, bad);
-        SA_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        SA_TRY(readback(&hbad, bad, sizeof hbad, st));
+        SA_TRY(sync_stream(st));
         if (hbad != ~0ull) {
             err_state().bad = (int64_t)hbad;
             return set_error(SA_ERR_DEGENERATE, "simplex %lld is degenerate (zero volume)", (long long)hbad);
@@ -1812,8 +1812,8 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
         SA_LAUNCH(k_inc_count<D>, ge, B, 0, st, (const I *)M->me, M->nme, P->node_begin, P->node_end,
                   (unsigned long long *)cnt);
     SA_TRY(exclusive_scan_i64(cnt, P->inc_ptr, nn, P->scan_tmp, st));
-    SA_CUDA_TRY(cudaMemcpyAsync(&P->n_inc, P->inc_ptr + nn, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SA_CUDA_TRY(cudaStreamSynchronize(st));
+    SA_TRY(readback(&P->n_inc, P->inc_ptr + nn, sizeof(int64_t), st));
+    SA_TRY(sync_stream(st));
     SA_CUDA_TRY(cudaMallocAsync((void **)&P->inc, std::max<int64_t>(P->n_inc, 1) * sizeof(uint2), st));
     SA_CUDA_TRY(cudaMemsetAsync(cnt, 0, (nn + 1) * sizeof(int64_t), st));
     if (M->nme)
@@ -1831,15 +1831,15 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
         SA_LAUNCH(k_max_diff, std::min<int64_t>(grid_for(nn, 256), 148 * 8), 256, 0, st, P->inc_ptr, nn,
                   (unsigned long long *)(P->counters + 6));
         int64_t mi = 0;
-        SA_CUDA_TRY(cudaMemcpyAsync(&mi, P->counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        SA_TRY(readback(&mi, P->counters + 6, sizeof(int64_t), st));
+        SA_TRY(sync_stream(st));
         if (mi <= NS_CAPI) {
             SA_LAUNCH((k_node_symbolic<D, false>), grid_for(nn, NS_THREADS), NS_THREADS, 0, st, (const I *)M->me,
                       P->inc_ptr, P->inc, nn, cnt, (const int64_t *)nullptr, (int32_t *)nullptr,
                       (unsigned long long *)(P->counters + 7));
             int64_t ov = 0;
-            SA_CUDA_TRY(cudaMemcpyAsync(&ov, P->counters + 7, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-            SA_CUDA_TRY(cudaStreamSynchronize(st));
+            SA_TRY(readback(&ov, P->counters + 7, sizeof(int64_t), st));
+            SA_TRY(sync_stream(st));
             fast = ov == 0;   // else (a node with > NS_CAPC neighbours): the general kernels below
         }
     }
@@ -1852,8 +1852,8 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
         SA_CUDA_TRY(cudaMemsetAsync(P->counters + 5, 0, 2 * sizeof(int64_t), st));
         SA_LAUNCH(k_node_cols<D>, grid_for(nn, 128), 128, 0, st, (const I *)M->me, P->inc_ptr, P->inc, nn, cnt,
                   (const int64_t *)nullptr, (int32_t *)nullptr, (unsigned long long *)(P->counters + 5), hsym);
-        SA_CUDA_TRY(cudaMemcpyAsync(&nhsym, P->counters + 5, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        SA_TRY(readback(&nhsym, P->counters + 5, sizeof(int64_t), st));
+        SA_TRY(sync_stream(st));
         if (nhsym) {
             SA_CUDA_TRY(cudaFuncSetAttribute(k_heavy_cols<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm));
             SA_LAUNCH(k_heavy_cols<D>, (unsigned)nhsym, 1024, hsm, st, (const I *)M->me, P->inc_ptr, P->inc, hsym, cnt,
@@ -1862,9 +1862,9 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
     }
     SA_TRY(exclusive_scan_i64(cnt, P->colptr, nn, P->scan_tmp, st));
     int64_t too_big = 0;
-    SA_CUDA_TRY(cudaMemcpyAsync(&P->n_colnodes, P->colptr + nn, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    if (nhsym) SA_CUDA_TRY(cudaMemcpyAsync(&too_big, P->counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SA_CUDA_TRY(cudaStreamSynchronize(st));
+    SA_TRY(readback(&P->n_colnodes, P->colptr + nn, sizeof(int64_t), st));
+    if (nhsym) SA_TRY(readback(&too_big, P->counters + 6, sizeof(int64_t), st));
+    SA_TRY(sync_stream(st));
     if (too_big) {
         SA_CUDA_TRY(cudaFreeAsync(hsym, st));
         return set_error(SA_ERR_CAPACITY, "a node has more than %d vertex references in its incident elements",
@@ -1891,8 +1891,8 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
         SA_LAUNCH(k_max_diff, std::min<int64_t>(grid_for(nn, 256), 148 * 8), 256, 0, st, P->colptr, nn,
                   (unsigned long long *)(P->counters + 6));
     int64_t md = 0;
-    SA_CUDA_TRY(cudaMemcpyAsync(&md, P->counters + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SA_CUDA_TRY(cudaStreamSynchronize(st));
+    SA_TRY(readback(&md, P->counters + 6, sizeof(int64_t), st));
+    SA_TRY(sync_stream(st));
     P->max_deg = md;
     const int m = P->m;
     // light / heavy rows: the row kernels size their shared-memory
@@ -1911,8 +1911,8 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
             SA_LAUNCH(k_heavy_rows_list, std::min<int64_t>(grid_for(nn, 256), 148 * 8), 256, 0, st, P->colptr, nn, cap,
                       P->heavy_rows, (unsigned long long *)(P->counters + 6));
             int64_t h[2];
-            SA_CUDA_TRY(cudaMemcpyAsync(h, P->counters + 6, sizeof h, cudaMemcpyDeviceToHost, st));
-            SA_CUDA_TRY(cudaStreamSynchronize(st));
+            SA_TRY(readback(h, P->counters + 6, sizeof h, st));
+            SA_TRY(sync_stream(st));
             P->n_heavy = h[0];
             P->light_deg = h[1];
         }
@@ -1925,7 +1925,7 @@ int symbolic_kernels(sa_plan *P, cudaStream_t st)
     SA_CUDA_TRY(cudaMallocAsync((void **)&P->indices, std::max<int64_t>(P->nnz, 1) * sizeof(int32_t), st));
     SA_LAUNCH(k_dof_csr, grid_for(nn + 1, 128), 128, 0, st, P->colptr, P->cols, nn, m, P->indptr, P->indices);
     SA_CUDA_TRY(cudaFreeAsync(cnt, st));
-    SA_CUDA_TRY(cudaStreamSynchronize(st));
+    SA_TRY(sync_stream(st));
     return SA_OK;
 }
 
@@ -1950,8 +1950,8 @@ int build_winc(sa_plan *P, cudaStream_t st)
         SA_LAUNCH(k_warp_span, grid_for(nw, 128), 128, 0, st, P->inc_ptr, nn, span);
         SA_TRY(exclusive_scan_i64(span, P->wseg, nw, P->scan_tmp, st));
     }
-    SA_CUDA_TRY(cudaMemcpyAsync(&P->n_winc, P->wseg + nw, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    SA_CUDA_TRY(cudaStreamSynchronize(st));
+    SA_TRY(readback(&P->n_winc, P->wseg + nw, sizeof(int64_t), st));
+    SA_TRY(sync_stream(st));
     SA_CUDA_TRY(cudaFreeAsync(span, st));
     SA_CUDA_TRY(cudaMallocAsync((void **)&P->winc, std::max<int64_t>(P->n_winc, 1) * sizeof(IncRec), st));
     // padding records (rows shorter than their warp's longest) = all ones: ea = 0xffffffff sentinel
@@ -2466,8 +2466,8 @@ static int ensure_twopass(sa_plan *P, int kstride, bool batches, cudaStream_t st
         if (P->n_inc)
             SA_LAUNCH(k_inc_erange, std::min<int64_t>(grid_for(P->n_inc, 256), 148 * 8), 256, 0, st, P->inc,
                       P->n_inc, dr);
-        SA_CUDA_TRY(cudaMemcpyAsync(h, dr, sizeof h, cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        SA_TRY(readback(h, dr, sizeof h, st));
+        SA_TRY(sync_stream(st));
         SA_CUDA_TRY(cudaFreeAsync(dr, st));
         P->e_lo = P->n_inc ? (int64_t)h[0] : 0;
         P->e_hi = P->n_inc ? (int64_t)h[1] + 1 : 0;
@@ -2481,8 +2481,8 @@ static int ensure_twopass(sa_plan *P, int kstride, bool batches, cudaStream_t st
             SA_TRY(exclusive_scan_i64(span, P->wseg, nw, P->scan_tmp, st));
             SA_CUDA_TRY(cudaFreeAsync(span, st));
         }
-        SA_CUDA_TRY(cudaMemcpyAsync(&P->tp_nslots, P->wseg + nw, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        SA_TRY(readback(&P->tp_nslots, P->wseg + nw, sizeof(int64_t), st));
+        SA_TRY(sync_stream(st));
         if (P->tp_nslots >= 0xffffffffLL)
             return set_error(SA_ERR_CAPACITY, "two-pass numeric: %lld slots overflow 32-bit slot indices",
                              (long long)P->tp_nslots);
@@ -2505,8 +2505,8 @@ static int ensure_twopass(sa_plan *P, int kstride, bool batches, cudaStream_t st
             SA_LAUNCH(k_eb_build<3>, (unsigned)nb, EB_SIZE, 0, st, (const int4 *)P->mesh->me, P->e_lo, ne, P->eb_verts,
                       P->eb_count, P->eb_loc, mx);
         unsigned long long h = 0;
-        SA_CUDA_TRY(cudaMemcpyAsync(&h, mx, sizeof h, cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        SA_TRY(readback(&h, mx, sizeof h, st));
+        SA_TRY(sync_stream(st));
         SA_CUDA_TRY(cudaFreeAsync(mx, st));
         P->eb_maxn = (int)std::min<unsigned long long>(h, EB_CAP);
         P->eb_allfit = h <= EB_CAP;
@@ -2633,8 +2633,8 @@ int sa_numeric(sa_plan *P, int ops, const sa_coeffs *cf, double *const *vals_dev
     if (rc != SA_OK) return rc;
     if (n_zero_out) {
         int64_t h[8];
-        SA_CUDA_TRY(cudaMemcpyAsync(h, P->counters, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        SA_TRY(readback(h, P->counters, 8 * sizeof(int64_t), st));
+        SA_TRY(sync_stream(st));
         if (h[7]) return set_error(SA_ERR_CUDA, "chunk kernel: a carry wait timed out (internal error)");
         for (int o = 0; o < nout; ++o) n_zero_out[o] = h[o];
         if (h[4] != 0x7f7f7f7f7f7f7f7fLL) {

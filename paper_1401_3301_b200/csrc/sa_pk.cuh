@@ -200,8 +200,8 @@ int sa_pk_plan_create(int ndfe, int64_t nq, int64_t nme, const int64_t *me_dev, 
         if (nm) SA_LAUNCH(k_pk_pack, std::min<int64_t>(grid_for(nm, 256), 148 * 32), 256, 0, st, me_dev, nm, nq, P->me,
                           c + 3);
         int64_t h[4];
-        SA_CUDA_TRY(cudaMemcpyAsync(h, P->counters, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        SA_TRY(readback(h, P->counters, 4 * sizeof(int64_t), st));
+        SA_TRY(sync_stream(st));
         if (h[3] != -1) {
             err_state().bad = h[3];
             return set_error(SA_ERR_INDEX_RANGE, "connectivity entry me[%lld, %lld] out of range [0, %lld)",
@@ -210,8 +210,8 @@ int sa_pk_plan_create(int ndfe, int64_t nq, int64_t nme, const int64_t *me_dev, 
         SA_CUDA_TRY(cudaMemsetAsync(cnt, 0, (nq + 1) * sizeof(int64_t), st));
         if (nme) SA_LAUNCH(k_pk_count, grid_for(nme, 128), 128, 0, st, P->me, ndfe, nme, (unsigned long long *)cnt);
         SA_TRY(exclusive_scan_i64(cnt, P->inc_ptr, nq, P->scan_tmp, st));
-        SA_CUDA_TRY(cudaMemcpyAsync(&P->n_inc, P->inc_ptr + nq, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        SA_TRY(readback(&P->n_inc, P->inc_ptr + nq, sizeof(int64_t), st));
+        SA_TRY(sync_stream(st));
         SA_CUDA_TRY(cudaMallocAsync((void **)&P->inc, std::max<int64_t>(P->n_inc, 1) * sizeof(uint2), st));
         SA_CUDA_TRY(cudaMallocAsync((void **)&P->rank, std::max<int64_t>(P->n_inc * ndfe, 1), st));
         SA_CUDA_TRY(cudaMemsetAsync(cnt, 0, (nq + 1) * sizeof(int64_t), st));
@@ -224,9 +224,9 @@ int sa_pk_plan_create(int ndfe, int64_t nq, int64_t nme, const int64_t *me_dev, 
         }
         SA_TRY(exclusive_scan_i64(cnt, P->colptr, nq, P->scan_tmp, st));
         if (nq) SA_LAUNCH(k_max_diff, std::min<int64_t>(grid_for(nq, 256), 148 * 8), 256, 0, st, P->colptr, nq, c + 2);
-        SA_CUDA_TRY(cudaMemcpyAsync(h, P->counters, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaMemcpyAsync(&P->nnz, P->colptr + nq, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        SA_TRY(readback(h, P->counters, 4 * sizeof(int64_t), st));
+        SA_TRY(readback(&P->nnz, P->colptr + nq, sizeof(int64_t), st));
+        SA_TRY(sync_stream(st));
         if (h[1]) return set_error(SA_ERR_CAPACITY, "a lattice node has more than 255 distinct neighbours");
         if (P->nnz >= ((int64_t)1 << 31)) return set_error(SA_ERR_CAPACITY, "int32 column indices overflow");
         P->max_deg = h[2];
@@ -234,7 +234,7 @@ int sa_pk_plan_create(int ndfe, int64_t nq, int64_t nme, const int64_t *me_dev, 
         if (nq) SA_LAUNCH(k_pk_cols, grid_for(nq, 128), 128, 0, st, P->me, ndfe, nme, P->inc_ptr, P->inc, nq, cnt,
                           (const int64_t *)P->colptr, P->cols, P->rank, c + 1);
         SA_CUDA_TRY(cudaFreeAsync(cnt, st));
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        SA_TRY(sync_stream(st));
         return SA_OK;
     };
     const int rc = run();
@@ -277,8 +277,8 @@ int sa_pk_mass(sa_pk_plan *P, const double *cs_dev, const double *vols_dev, doub
         SA_LAUNCH(k_pk_mass, grid_for(P->nq, block), block, smem, st, P->inc_ptr, P->inc, P->rank, P->colptr,
                   P->ndfe, P->nq, cs_dev, vols_dev, vals_dev, (unsigned long long *)P->counters);
     if (n_zero_out) {
-        SA_CUDA_TRY(cudaMemcpyAsync(n_zero_out, P->counters, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        SA_CUDA_TRY(cudaStreamSynchronize(st));
+        SA_TRY(readback(n_zero_out, P->counters, sizeof(int64_t), st));
+        SA_TRY(sync_stream(st));
     }
     return SA_OK;
 }

@@ -1,5 +1,6 @@
 // sa_scan.cu -- device-wide exclusive scan (int64) and error plumbing.
 #include <cstdarg>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -45,8 +46,11 @@ bool tune_is(const char *key, const char *value)
     return v && n == strlen(value) && strncmp(v, value, n) == 0;
 }
 
+static void readback_drop_pending();
+
 int set_error(int status, const char *fmt, ...)
 {
+    readback_drop_pending();   // an error return must not leave read-backs aimed at a dead frame
     char buf[1024];
     va_list ap;
     va_start(ap, fmt);
@@ -54,6 +58,73 @@ int set_error(int status, const char *fmt, ...)
     va_end(ap);
     err_state().msg = buf;
     return status;
+}
+
+// ---- read-backs through mapped pinned memory (sa_common.cuh) ---------------
+namespace {
+__global__ void k_readback(const unsigned long long *__restrict__ src, unsigned long long *__restrict__ dst, int nwords)
+{
+    for (int i = threadIdx.x; i < nwords; i += blockDim.x) dst[i] = src[i];
+}
+
+struct ReadbackState {
+    unsigned char *staging = nullptr;   // mapped pinned, RB_BYTES
+    size_t used = 0;
+    struct Item { void *dst; size_t off, n; };
+    Item items[64];
+    int nitems = 0;
+};
+constexpr size_t RB_BYTES = 4096;
+ReadbackState &rb_state()
+{
+    static thread_local ReadbackState s;
+    return s;
+}
+}  // namespace
+
+static void readback_drop_pending()
+{
+    ReadbackState &r = rb_state();
+    r.nitems = 0;
+    r.used = 0;
+}
+
+int readback(void *host_dst, const void *dev_src, size_t bytes, cudaStream_t st)
+{
+    ReadbackState &r = rb_state();
+    if (!r.staging) {
+        void *p = nullptr;
+        if (cudaHostAlloc(&p, RB_BYTES, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+        }
+        r.staging = (unsigned char *)p;
+    }
+    if (!r.staging || bytes == 0 || bytes % 8 != 0 || ((uintptr_t)dev_src & 7) || r.used + bytes > RB_BYTES ||
+        r.nitems == 64) {
+        SA_CUDA_TRY(cudaMemcpyAsync(host_dst, dev_src, bytes, cudaMemcpyDeviceToHost, st));
+        return SA_OK;
+    }
+    k_readback<<<1, 32, 0, st>>>((const unsigned long long *)dev_src, (unsigned long long *)(r.staging + r.used),
+                                 (int)(bytes / 8));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(SA_ERR_CUDA, "read-back launch failed: %s", cudaGetErrorString(e));
+    r.items[r.nitems++] = {host_dst, r.used, bytes};
+    r.used += bytes;
+    return SA_OK;
+}
+
+int sync_stream(cudaStream_t st)
+{
+    ReadbackState &r = rb_state();
+    cudaError_t e = cudaStreamSynchronize(st);
+    // (delivered even after an error: the caller reports it)
+    for (int i = 0; i < r.nitems; ++i) memcpy(r.items[i].dst, r.staging + r.items[i].off, r.items[i].n);
+    r.nitems = 0;
+    r.used = 0;
+    if (e != cudaSuccess)
+        return set_error(SA_ERR_CUDA, "cudaStreamSynchronize failed: %s", cudaGetErrorString(e));
+    return SA_OK;
 }
 
 namespace {
