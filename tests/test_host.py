@@ -270,3 +270,20 @@ def test_general_kernel_column_compaction_roundtrip():
         for j in range(16):
             full[:, j] = cols[:, colmap[j]] if colmap[j] >= 0 else consts[j]
         assert np.array_equal(full, k.packed())
+
+
+def test_host_thread_pool_widens_indices():
+    # sa_host_widen_i32 runs on the library's parked host thread pool (no GPU
+    # involved): repeated calls with varying thread counts, sizes and offsets
+    import ctypes
+
+    from paper_1401_3301_b200 import _lib
+
+    L = _lib.load()
+    rng = np.random.default_rng(3)
+    for n, nthreads, off in [(0, 4, 0), (1, 8, 5), (65537, 3, 0), (1 << 20, 16, 1 << 33), (999983, 64, -7), (12345, 1, 0)]:
+        src = rng.integers(-(1 << 31), 1 << 31, n, dtype=np.int64).astype(np.int32)
+        dst = np.full(n, -1, dtype=np.int64)
+        rc = L.sa_host_widen_i32(ctypes.c_void_p(src.ctypes.data), n, off, ctypes.c_void_p(dst.ctypes.data), nthreads)
+        assert rc == 0
+        assert np.array_equal(dst, src.astype(np.int64) + off)
